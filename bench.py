@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark of the numerical-entanglement hot path on B200 (driver contract).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+M=3 streams of N=2^24 int32 samples in [-2^11, 2^11-1], one 256-tap filter,
+geometry derive_params(3, 64) = (l=21, k=21); full linear convolution of every
+entangled stream, all 3 outputs recovered (failed=None pivots on stream 0 and
+checks the redundant stream).  One step = one pass of the fused
+entangle -> conv -> extract kernel over the whole batch, inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N>1 (torchrun): halo-split weak scaling -- rank p owns a 2^24-sample slice of
+an N*2^24-sample signal; the K-1 = 255-sample halo comes from rank p-1 over
+NCCL once at setup; the timed region has no collective.  Rank 0 prints one
+JSON line.  --impl reference times the reference algorithm's CPU restatement
+(oracle/, all host threads) on the same workload; only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "entangled int conv output samples/s; overhead vs non-entangled conv (%)"
+UNIT = "samples/s"
+WORKLOAD = "cfg2: M=3, N=2^24 int32 in [-2^11,2^11), K=256 taps, (m,w,l,k)=(3,64,21,21), full conv"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").tobytes()).hexdigest()
+
+
+# ----------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- workload --
+
+def make_inputs(rank: int, world: int, n: int, K: int):
+    """Rank 0 holds the canonical cfg2 draw (seed 2); rank p > 0 draws its
+    slice from seed (2, p) -- same shapes and value distribution."""
+    from paper_1509_03838_b200 import workloads
+
+    if rank == 0:
+        wl = workloads.make(2, n=n, K=K)
+        return wl.params, wl.c, wl.g
+    rng = np.random.default_rng([2, rank])
+    c = rng.integers(-(1 << 11), 1 << 11, (3, n), dtype=np.int64)
+    g = workloads.make(2, n=16, K=K).g  # every rank uses the same filter
+    return workloads.make(2, n=16, K=K).params, c, g
+
+
+# ------------------------------------------------------------ our device path --
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_03838_b200 as nent
+    from paper_1509_03838_b200 import _device as D
+    from paper_1509_03838_b200 import fused
+    from paper_1509_03838_b200._lib import MAC_F64, MAC_G64, MAC_I32, MAC_NAMES, MAC_S64, MAC_W64
+    from paper_1509_03838_b200.hostpath import ChunkedEntangledConv
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, K = 1 << 24, 256
+    params, c_np, g = make_inputs(rank, world, n, K)
+    m = params.m
+    H = K - 1
+    c_dev = torch.from_numpy(c_np).to(dev).to(torch.int32)
+    # halo-split: the K-1 samples left of this rank's slice come from rank-1
+    if world > 1:
+        halo = torch.zeros((m, H), dtype=torch.int32, device=dev)
+        ops = []
+        if rank + 1 < world:
+            ops.append(dist.P2POp(dist.isend, c_dev[:, n - H:].contiguous(), rank + 1))
+        if rank > 0:
+            ops.append(dist.P2POp(dist.irecv, halo, rank - 1))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        x_dev = torch.cat([halo, c_dev], dim=1).contiguous()
+        last = rank == world - 1  # the last rank also owns the K-1 tail outputs
+        n_out = n + (H if last else 0)
+        period, n_in, y_begin = H + n + H, H + n, H  # rank 0 keeps a zero halo (left edge)
+    else:
+        x_dev = c_dev
+        n_out, period, n_in, y_begin = n + H, n + H, n, 0
+
+    max_c = (1 << 11)
+    eps_bound = max_c * ((1 << params.l) + 1)
+    flavor = fused.conv_flavor(eps_bound, g)           # F64 for cfg2 (|delta| < 2^53)
+    plain_flavor_same = flavor                          # same accumulator width
+    plain_flavor_narrow = fused.conv_flavor(max_c, g)   # narrowest exact plain kernel (I32)
+    g_dev = D.taps_tensor(g, flavor)
+    d_dev = torch.empty((m, n_out), dtype=torch.int32, device=dev)
+    y_plain = torch.empty((m, n_out), dtype=torch.int32, device=dev)
+    mismatch = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        D.fused_conv(x_dev, g_dev, K, params.l, flavor, None, params.w > 32, period, n_in=n_in,
+                     y_begin=y_begin, n_out=n_out, out=d_dev, mismatch=mismatch)
+
+    def plain(fl, gd):
+        D.conv(x_dev, gd, K, fl, period=period, y_begin=y_begin, n_out=n_out, out=y_plain)
+
+    g_plain_narrow = D.taps_tensor(g, plain_flavor_narrow)
+
+    for _ in range(args.warmup):
+        step()
+        plain(plain_flavor_same, g_dev)
+        plain(plain_flavor_narrow, g_plain_narrow)
+    torch.cuda.synchronize(dev)
+
+    # parity of the benchmarked output itself (rank 0 holds the canonical cfg2)
+    exact = None
+    if rank == 0 and world == 1:
+        known = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())["cfg2"]["d"]
+        exact = sha(d_dev.to(torch.int64).cpu().numpy()) == known and int(mismatch.item()) == 0
+
+    # ---------------- timed region: exactly K steps ----------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_step = ms_max / args.steps
+    samples_job = m * n_out * world if world == 1 else m * (n * world + H)
+    value = samples_job / (ms_step / 1e3)
+
+    # ---------------- interleaved overhead vs plain conv ----------------
+    def timed(fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        return a, b
+
+    pairs = []
+    for _ in range(max(5, min(args.steps, 15))):
+        e = timed(step)
+        ps = timed(lambda: plain(plain_flavor_same, g_dev))
+        pn = timed(lambda: plain(plain_flavor_narrow, g_plain_narrow))
+        pairs.append((e, ps, pn))
+    torch.cuda.synchronize(dev)
+    t_e = [a.elapsed_time(b) for (a, b), _, _ in pairs]
+    t_s = [a.elapsed_time(b) for _, (a, b), _ in pairs]
+    t_n = [a.elapsed_time(b) for _, _, (a, b) in pairs]
+    ovh_same = statistics.median([(x - y) / y * 100 for x, y in zip(t_e, t_s)])
+    ovh_narrow = statistics.median([(x - y) / y * 100 for x, y in zip(t_e, t_n)])
+
+    # ---------------- measured MAC-pipe peaks (roofline denominators) ----------------
+    peaks = {}
+    for kind in (MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64):
+        D.microbench(kind, 148 * 4, 256, 64)  # warm
+        best = 0.0
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            macs = D.microbench(kind, 148 * 8, 256, 4096)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            best = max(best, macs / (a.elapsed_time(b) / 1e3))
+        peaks[MAC_NAMES[kind]] = best
+    kern_ms = statistics.median(t_e)  # one fused launch per step, measured on its stream
+    macs_launch = m * n * K  # algorithmic MACs per launch (M*N*K)
+    achieved_tflops = 2 * macs_launch / (kern_ms / 1e3) / 1e12
+    fname = MAC_NAMES[flavor]
+    peak_tflops = 2 * peaks[fname] / 1e12
+    traffic = None
+    tf = REPO / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("fused_conv_cfg2", {}).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---------------- e2e through the host-buffer path ----------------
+    e2e = None
+    if world == 1:
+        pipe = ChunkedEntangledConv(params, n, g, flavor, chunk=1 << 21)
+        c_host = torch.from_numpy(c_np.astype(np.int32)).pin_memory()
+        d_host = torch.empty((m, n + H), dtype=torch.int32).pin_memory()
+        for _ in range(2):
+            pipe.run(c_host, d_host)
+            pipe.synchronize()
+        torch.cuda.synchronize(dev)
+        if exact is not None:
+            exact = exact and sha(d_host.to(torch.int64).numpy()) == known
+        reps = max(3, min(args.steps, 8))
+        t0 = time.perf_counter()
+        launches_e2e = 0
+        for _ in range(reps):
+            launches_e2e += pipe.run(c_host, d_host)
+            pipe.synchronize()
+        torch.cuda.synchronize(dev)
+        e2e_s = (time.perf_counter() - t0) / reps
+        e2e = {"value": m * (n + H) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes(),
+               "d2h_bytes_per_step": pipe.d2h_bytes(), "ms_per_step": e2e_s * 1e3,
+               "path": "ChunkedEntangledConv: pinned int32 host -> 3-stream chunked H2D/fused kernel/D2H",
+               "kernels_per_step": launches_e2e // reps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(c_np, g, params, args.cpu_seconds)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": MAC_NAMES[flavor] + " exact (int32 in/out)",
+            "data": "synthetic (canonical seeded cfg2 draw, SURVEY.md 8d)",
+            "config": {"workload": WORKLOAD, "samples_per_step": samples_job,
+                       "parallelism": "halo-split" if world > 1 else "single GPU",
+                       "l2": "inputs 201 MB + outputs 201 MB per step > 126 MB L2; no flush needed",
+                       "mac_flavor": fname, "failed": None, "verify_redundant_stream": True},
+            "overhead_pct": ovh_same,
+            "overhead": {"vs_same_width_plain_pct": ovh_same,
+                         "vs_narrowest_plain_pct": ovh_narrow,
+                         "plain_same_flavor": MAC_NAMES[plain_flavor_same],
+                         "plain_narrow_flavor": MAC_NAMES[plain_flavor_narrow],
+                         "ms_entangled": statistics.median(t_e), "ms_plain_same": statistics.median(t_s),
+                         "ms_plain_narrow": statistics.median(t_n)},
+            "roofline": {"bound": "fp64", "pipe": "DFMA on CUDA cores (exact: |delta| < 2^53)",
+                         "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved_tflops / peak_tflops if peak_tflops else None,
+                         "traffic": traffic, "kernel": "nent::conv_tile_kernel<F64,3,fused>",
+                         "algorithmic_macs_per_launch": macs_launch,
+                         "peak_source": "measured in this run by nent_microbench (16 independent "
+                                        "accumulator chains per thread, 148*8 CTAs x 256 threads)",
+                         "peaks_measured_gmac_s": {k: v / 1e9 for k, v in peaks.items()}},
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "exact": exact,
+            "mismatches": int(mismatch.item()),
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------- CPU baseline --
+
+def cpu_pipeline_time(O, c: np.ndarray, g: np.ndarray, params, threads: int = 0):
+    """Reference algorithm on the CPU: entangle -> full conv on entangled
+    streams -> recover all 3 (failed=None), plus the plain conv."""
+    K = len(g)
+    t0 = time.perf_counter()
+    pad = np.zeros((c.shape[0], c.shape[1] + K - 1), dtype=np.int64)
+    pad[:, : c.shape[1]] = c
+    eps = O.entangle(pad, params.l, threads)
+    delta = O.circ_conv(eps, g, threads, wide=False)
+    d = O.disentangle(delta, params.m, params.l, params.w, None, threads)
+    t_ent = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    y = O.circ_conv(pad, g, threads, wide=False)
+    t_plain = time.perf_counter() - t0
+    assert np.array_equal(d, y)
+    return t_ent, t_plain, d.shape[0] * d.shape[1]
+
+
+def cpu_baseline(c, g, params, target_s: float):
+    from oracle import oracle as O
+
+    threads = O.max_threads()
+    ns = 1 << 16
+    t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params)
+    ns = int(min(c.shape[1], max(ns, ns * target_s / 2 / max(t, 1e-6))))
+    t_ent, t_plain, samples = cpu_pipeline_time(O, c[:, :ns], g, params)
+    import platform
+    model = ""
+    try:
+        model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
+                      if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"value": samples / t_ent, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {ns} samples of each of the 3 cfg2 streams, K=256, full conv "
+                      f"(entangle + conv + recover), oracle/nent_oracle.c OpenMP",
+            "plain_value": samples / t_plain,
+            "overhead_pct": (t_ent - t_plain) / t_plain * 100,
+            "seconds": t_ent + t_plain, "host": f"{model} ({os.cpu_count()} logical CPUs, {platform.machine()})"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return  # only rank 0 runs the CPU reference arm
+    from oracle import oracle as O
+
+    params, c, g = make_inputs(0, 1, 1 << 24, 256)
+    threads = O.max_threads()
+    # bounded sample per step, sized so the whole run stays within a few minutes
+    ns = 1 << 16
+    t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params, threads)
+    budget = 150.0 / max(args.steps + args.warmup, 1)
+    ns = int(min(c.shape[1], max(ns, ns * budget / 2 / max(t, 1e-6))))
+    for _ in range(args.warmup):
+        cpu_pipeline_time(O, c[:, :ns], g, params, threads)
+    te, tp = [], []
+    for _ in range(args.steps):
+        a, b, samples = cpu_pipeline_time(O, c[:, :ns], g, params, threads)
+        te.append(a)
+        tp.append(b)
+    t_step = sum(te) / len(te)
+    value = samples / t_step
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64 (reference numpy semantics)",
+        "data": "synthetic (canonical seeded cfg2 draw, SURVEY.md 8d)",
+        "config": {"workload": WORKLOAD, "sample": f"first {ns} samples per stream"},
+        "impl": "reference",
+        "overhead_pct": statistics.median([(a - b) / b * 100 for a, b in zip(te, tp)]),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"first {ns} samples of each cfg2 stream per step (K=256, full "
+                                   f"conv, entangle+conv+recover), oracle/nent_oracle.c OpenMP"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,388 @@
+// codec.cu -- K1 entangle, K3 extract/recover, poison, range/bound reductions,
+// checksum baseline.  HBM-bound elementwise passes: grid-stride, coalesced,
+// several independent loads in flight per thread.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+#include "recover.cuh"
+
+namespace nent {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return NENT_ERR_CUDA;
+  }
+  return NENT_OK;
+}
+
+constexpr int EW_THREADS = 256;
+constexpr int EW_UNROLL = 4;
+
+// ---------------------------------------------------------------- entangle --
+// eps[i][j] = (src[(i-1) mod m][j] << l) + src[i][j]; optional first-offender.
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+entangle_kernel(const Rows src, MutRows eps, int m, int64_t n, int l, int64_t hi, int check,
+                unsigned long long* bad) {
+  const int i = blockIdx.y;
+  const TI* __restrict__ cur = reinterpret_cast<const TI*>(src.p[i]);
+  const TI* __restrict__ prv = reinterpret_cast<const TI*>(src.p[(i + m - 1) % m]);
+  TO* __restrict__ out = reinterpret_cast<TO*>(eps.p[i]);
+  const int64_t stride = (int64_t)gridDim.x * EW_THREADS * EW_UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * EW_THREADS * EW_UNROLL + threadIdx.x; base < n;
+       base += stride) {
+    int64_t a[EW_UNROLL], b[EW_UNROLL];
+#pragma unroll
+    for (int u = 0; u < EW_UNROLL; ++u) {
+      int64_t j = base + (int64_t)u * EW_THREADS;
+      a[u] = j < n ? (int64_t)__ldg(prv + j) : 0;
+      b[u] = j < n ? (int64_t)__ldg(cur + j) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < EW_UNROLL; ++u) {
+      int64_t j = base + (int64_t)u * EW_THREADS;
+      if (j < n) {
+        out[j] = (TO)(uint64_t)wadd(wshl(a[u], l), b[u]);
+        if (check && wabs(b[u]) > hi) atomicMin(bad, (unsigned long long)((int64_t)i * n + j));
+      }
+    }
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+shift_add_kernel(const TI* __restrict__ a, const TI* __restrict__ b, TO* __restrict__ out,
+                 int64_t n, int l) {
+  for (int64_t j = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * EW_THREADS)
+    out[j] = (TO)(uint64_t)wadd(wshl((int64_t)__ldg(a + j), l), (int64_t)__ldg(b + j));
+}
+
+// ----------------------------------------------------------------- extract --
+// One thread per position; reads the m-1 surviving rows once, writes m rows.
+template <int MT, typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+extract_kernel(const Rows delta, MutRows out, int m, int64_t n, int l, int r, int wide,
+               unsigned long long* overflow) {
+  constexpr int CAP = MT > 0 ? MT : NENT_MAX_STREAMS;
+  const int M = MT > 0 ? MT : m;
+  for (int64_t j = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * EW_THREADS) {
+    int64_t rot[CAP], orot[CAP];
+#pragma unroll
+    for (int t = 0; t < M - 1; ++t) {
+      int row = r + 1 + t;
+      row -= row >= M ? M : 0;
+      row -= row >= M ? M : 0;
+      rot[t] = (int64_t)__ldg(reinterpret_cast<const TI*>(delta.p[row]) + j);
+    }
+    bool ovf = recover_rot<MT>(rot, M, l, wide != 0, orot);
+    if (ovf && overflow) atomicAdd(overflow, 1ull);
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      int row = r + t;
+      row -= row >= M ? M : 0;
+      reinterpret_cast<TO*>(out.p[row])[j] = (TO)(uint64_t)orot[t];
+    }
+  }
+}
+
+// Independent m=3 recipe (codec.py:151-183).
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+extract_m3_kernel(const Rows delta, MutRows out, int64_t n, int l, int w, int r) {
+  const TI* a = reinterpret_cast<const TI*>(delta.p[(r + 1) % 3]);
+  const TI* b = reinterpret_cast<const TI*>(delta.p[(r + 2) % 3]);
+  for (int64_t j = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * EW_THREADS) {
+    int64_t av = (int64_t)__ldg(a + j), bv = (int64_t)__ldg(b + j);
+    int64_t d2, d0;
+    if (w <= 32) {
+      int64_t dt = wsub(bv, wshl(av, l));
+      if (w == 32) {
+        int up = 2 * (w - l);
+        d2 = (int64_t)((uint64_t)dt << up) >> up;
+      } else {
+        uint64_t mask = (((uint64_t)1) << (2 * l)) - 1, sb = ((uint64_t)1) << (2 * l - 1);
+        d2 = (int64_t)((((uint64_t)dt & mask) ^ sb) - sb);
+      }
+      d0 = wneg(wsub(dt, d2)) >> (2 * l);
+    } else {
+      typedef unsigned __int128 u128;
+      u128 dt = (u128)(__int128)bv - ((u128)(__int128)av << l);
+      u128 mask = (((u128)1) << (2 * l)) - 1, sb = ((u128)1) << (2 * l - 1);
+      u128 d2w = ((dt & mask) ^ sb) - sb;
+      d2 = (int64_t)(uint64_t)d2w;
+      d0 = (int64_t)((__int128)(d2w - dt) >> (2 * l));
+    }
+    reinterpret_cast<TO*>(out.p[(r + 2) % 3])[j] = (TO)(uint64_t)d2;
+    reinterpret_cast<TO*>(out.p[r])[j] = (TO)(uint64_t)d0;
+    reinterpret_cast<TO*>(out.p[(r + 1) % 3])[j] = (TO)(uint64_t)wsub(av, wshl(d0, l));
+  }
+}
+
+// ------------------------------------------------------------------ helpers --
+template <typename TO>
+__global__ void poison_kernel(TO* y, int64_t n, int w) {
+  const int64_t lo = (int64_t)(0 - ((uint64_t)1 << (w - 1)));
+  const int64_t hi = (int64_t)(((uint64_t)1 << (w - 1)) - 1);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    y[j] = (TO)(uint64_t)((j & 1) ? hi : lo);
+}
+
+template <typename TI>
+__global__ void __launch_bounds__(EW_THREADS)
+max_abs_kernel(const Rows x, int rows, int64_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int row = blockIdx.y; row < rows; row += gridDim.y) {
+    const TI* p = reinterpret_cast<const TI*>(x.p[row]);
+    for (int64_t j = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * EW_THREADS) {
+      unsigned long long a = uabs((int64_t)__ldg(p + j));
+      m = a > m ? a : m;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+    m = v > m ? v : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// First row-major index with |x| > hi (numpy's wrapping abs), as in
+// codec._check_input_range / checksum_encode (codec.py:34-46, checksum.py:42-55).
+template <typename TI>
+__global__ void __launch_bounds__(EW_THREADS)
+check_range_kernel(const Rows x, int64_t n, int64_t hi, unsigned long long* bad) {
+  const int row = blockIdx.y;
+  const TI* p = reinterpret_cast<const TI*>(x.p[row]);
+  for (int64_t j = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * EW_THREADS)
+    if (wabs((int64_t)__ldg(p + j)) > hi) atomicMin(bad, (unsigned long long)((int64_t)row * n + j));
+}
+
+template <typename TI, typename TO>
+__global__ void checksum_encode_kernel(const Rows x, int m, int64_t n, TO* cs) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t s = 0;
+    for (int i = 0; i < m; ++i) s += (uint64_t)(int64_t)__ldg(reinterpret_cast<const TI*>(x.p[i]) + j);
+    cs[j] = (TO)s;
+  }
+}
+
+template <typename TI, typename TC, typename TO>
+__global__ void checksum_recover_kernel(const Rows x, const TC* cs, int m, int64_t n, int failed,
+                                        TO* out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t s = (uint64_t)(int64_t)__ldg(cs + j);
+    for (int i = 0; i < m; ++i)
+      if (i != failed) s -= (uint64_t)(int64_t)__ldg(reinterpret_cast<const TI*>(x.p[i]) + j);
+    out[j] = (TO)s;
+  }
+}
+
+}  // namespace nent
+
+using namespace nent;
+
+extern "C" {
+
+const char* nent_last_error(void) { return g_err; }
+int nent_abi_version(void) { return NENT_ABI_VERSION; }
+
+int nent_device_ok(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { set_error("no CUDA device"); return 0; }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { set_error("cudaGetDeviceProperties failed"); return 0; }
+  if (prop.major != 10 || prop.minor != 0) {
+    set_error("library built for sm_100a, device is sm_%d%d", prop.major, prop.minor);
+    return 0;
+  }
+  cudaFuncAttributes attr;
+  if (cudaFuncGetAttributes(&attr, (const void*)poison_kernel<int64_t>) != cudaSuccess) {
+    set_error("kernel image not loadable: %s", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
+  return 1;
+}
+
+int nent_entangle(const void* const* src, int src_bits, void* const* eps, int eps_bits, int m,
+                  int64_t n, int l, int64_t check_hi, uint64_t* bad_index_dev, void* stream) {
+  NENT_CHECK_BITS(src_bits);
+  NENT_CHECK_BITS(eps_bits);
+  if (m < 1 || m > NENT_MAX_STREAMS || n < 0 || l < 0 || l > 63) {
+    set_error("entangle: bad geometry m=%d n=%lld l=%d", m, (long long)n, l);
+    return NENT_ERR_PARAM;
+  }
+  cudaStream_t s = as_stream(stream);
+  int check = check_hi >= 0 && bad_index_dev != nullptr;
+  if (check) cudaMemsetAsync(bad_index_dev, 0xff, sizeof(uint64_t), s);
+  if (n == 0) return NENT_OK;
+  Rows R = to_rows(src, m);
+  MutRows W = to_mrows(eps, m);
+  dim3 grid(grid_for(n, EW_THREADS, EW_UNROLL, 148 * 16 / (m > 4 ? 4 : 1)), m);
+  DISPATCH_IO(src_bits, eps_bits,
+              (entangle_kernel<TI, TO><<<grid, EW_THREADS, 0, s>>>(
+                  R, W, m, n, l, check_hi, check, (unsigned long long*)bad_index_dev)));
+  return check_launch("entangle");
+}
+
+int nent_shift_add(const void* a, const void* b, int in_bits, void* out, int out_bits, int64_t n,
+                   int l, void* stream) {
+  NENT_CHECK_BITS(in_bits);
+  NENT_CHECK_BITS(out_bits);
+  if (n <= 0) return NENT_OK;
+  cudaStream_t s = as_stream(stream);
+  int grid = grid_for(n, EW_THREADS, 4);
+  DISPATCH_IO(in_bits, out_bits,
+              (shift_add_kernel<TI, TO><<<grid, EW_THREADS, 0, s>>>(
+                  (const TI*)a, (const TI*)b, (TO*)out, n, l)));
+  return check_launch("shift_add");
+}
+
+int nent_extract(const void* const* delta, int delta_bits, void* const* out, int out_bits, int m,
+                 int64_t n, int l, int r, int wide, unsigned long long* overflow_dev,
+                 void* stream) {
+  NENT_CHECK_BITS(delta_bits);
+  NENT_CHECK_BITS(out_bits);
+  if (m < 3 || m > NENT_MAX_STREAMS || r < 0 || r >= m || l < 1 || (m - 1) * l > 63) {
+    set_error("extract: bad geometry m=%d l=%d r=%d", m, l, r);
+    return NENT_ERR_PARAM;
+  }
+  if (n <= 0) return NENT_OK;
+  cudaStream_t s = as_stream(stream);
+  Rows D = to_rows(delta, m);
+  D.p[r] = nullptr;  // the failed stream is never dereferenced
+  MutRows O = to_mrows(out, m);
+  int grid = grid_for(n, EW_THREADS, 4);
+#define EXTRACT_CASE(MTV)                                                                  \
+  DISPATCH_IO(delta_bits, out_bits,                                                        \
+              (extract_kernel<MTV, TI, TO><<<grid, EW_THREADS, 0, s>>>(D, O, m, n, l, r, wide, \
+                                                                      overflow_dev)))
+  switch (m) {
+    case 3: EXTRACT_CASE(3); break;
+    case 4: EXTRACT_CASE(4); break;
+    case 5: EXTRACT_CASE(5); break;
+    case 8: EXTRACT_CASE(8); break;
+    default: EXTRACT_CASE(0); break;
+  }
+#undef EXTRACT_CASE
+  return check_launch("extract");
+}
+
+int nent_extract_m3(const void* const* delta, int delta_bits, void* const* out, int out_bits,
+                    int64_t n, int l, int w, int r, void* stream) {
+  NENT_CHECK_BITS(delta_bits);
+  NENT_CHECK_BITS(out_bits);
+  if (r < 0 || r > 2 || l < 1 || 2 * l > 63 + (w > 32 ? 64 : 0)) {
+    set_error("extract_m3: bad parameters");
+    return NENT_ERR_PARAM;
+  }
+  if (n <= 0) return NENT_OK;
+  cudaStream_t s = as_stream(stream);
+  Rows D = to_rows(delta, 3);
+  D.p[r] = nullptr;
+  MutRows O = to_mrows(out, 3);
+  int grid = grid_for(n, EW_THREADS, 4);
+  DISPATCH_IO(delta_bits, out_bits,
+              (extract_m3_kernel<TI, TO><<<grid, EW_THREADS, 0, s>>>(D, O, n, l, w, r)));
+  return check_launch("extract_m3");
+}
+
+int nent_poison(void* y, int y_bits, int64_t n, int w, void* stream) {
+  NENT_CHECK_BITS(y_bits);
+  if (w < 2 || w > 64) { set_error("poison: bad w=%d", w); return NENT_ERR_PARAM; }
+  if (n <= 0) return NENT_OK;
+  cudaStream_t s = as_stream(stream);
+  int grid = grid_for(n, 256, 4);
+  if (y_bits == 32) poison_kernel<int32_t><<<grid, 256, 0, s>>>((int32_t*)y, n, w);
+  else poison_kernel<int64_t><<<grid, 256, 0, s>>>((int64_t*)y, n, w);
+  return check_launch("poison");
+}
+
+int nent_max_abs(const void* const* x, int x_bits, int rows, int64_t n, uint64_t* out_dev,
+                 void* stream) {
+  NENT_CHECK_BITS(x_bits);
+  if (rows < 0 || rows > NENT_MAX_STREAMS) { set_error("max_abs: bad rows"); return NENT_ERR_PARAM; }
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(out_dev, 0, sizeof(uint64_t), s);
+  if (rows == 0 || n <= 0) return check_launch("max_abs");
+  Rows R = to_rows(x, rows);
+  dim3 grid(grid_for(n, EW_THREADS, 8, 148 * 8), rows);
+  if (x_bits == 32) max_abs_kernel<int32_t><<<grid, EW_THREADS, 0, s>>>(R, rows, n, (unsigned long long*)out_dev);
+  else max_abs_kernel<int64_t><<<grid, EW_THREADS, 0, s>>>(R, rows, n, (unsigned long long*)out_dev);
+  return check_launch("max_abs");
+}
+
+int nent_check_range(const void* const* x, int x_bits, int rows, int64_t n, int64_t hi,
+                     uint64_t* bad_index_dev, void* stream) {
+  NENT_CHECK_BITS(x_bits);
+  if (rows < 1 || rows > NENT_MAX_STREAMS || hi < 0) { set_error("check_range: bad arguments"); return NENT_ERR_PARAM; }
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(bad_index_dev, 0xff, sizeof(uint64_t), s);
+  if (n <= 0) return check_launch("check_range");
+  Rows R = to_rows(x, rows);
+  dim3 grid(grid_for(n, EW_THREADS, 4, 148 * 8), rows);
+  if (x_bits == 32) check_range_kernel<int32_t><<<grid, EW_THREADS, 0, s>>>(R, n, hi, (unsigned long long*)bad_index_dev);
+  else check_range_kernel<int64_t><<<grid, EW_THREADS, 0, s>>>(R, n, hi, (unsigned long long*)bad_index_dev);
+  return check_launch("check_range");
+}
+
+int nent_checksum_encode(const void* const* x, int x_bits, int m, int64_t n, void* cs,
+                         int cs_bits, void* stream) {
+  NENT_CHECK_BITS(x_bits);
+  NENT_CHECK_BITS(cs_bits);
+  if (m < 1 || m > NENT_MAX_STREAMS) { set_error("checksum_encode: bad m"); return NENT_ERR_PARAM; }
+  if (n <= 0) return NENT_OK;
+  cudaStream_t s = as_stream(stream);
+  Rows R = to_rows(x, m);
+  int grid = grid_for(n, 256, 4);
+  DISPATCH_IO(x_bits, cs_bits,
+              (checksum_encode_kernel<TI, TO><<<grid, 256, 0, s>>>(R, m, n, (TO*)cs)));
+  return check_launch("checksum_encode");
+}
+
+int nent_checksum_recover(const void* const* x, int x_bits, const void* cs, int cs_bits, int m,
+                          int64_t n, int failed, void* out, int out_bits, void* stream) {
+  NENT_CHECK_BITS(x_bits);
+  NENT_CHECK_BITS(cs_bits);
+  NENT_CHECK_BITS(out_bits);
+  if (m < 1 || m > NENT_MAX_STREAMS || failed < 0 || failed >= m) {
+    set_error("checksum_recover: bad failed=%d for m=%d", failed, m);
+    return NENT_ERR_PARAM;
+  }
+  if (n <= 0) return NENT_OK;
+  cudaStream_t s = as_stream(stream);
+  Rows R = to_rows(x, m);
+  R.p[failed] = nullptr;
+  int grid = grid_for(n, 256, 4);
+  if (cs_bits == 64) {
+    DISPATCH_IO(x_bits, out_bits,
+                (checksum_recover_kernel<TI, int64_t, TO><<<grid, 256, 0, s>>>(
+                    R, (const int64_t*)cs, m, n, failed, (TO*)out)));
+  } else {
+    DISPATCH_IO(x_bits, out_bits,
+                (checksum_recover_kernel<TI, int32_t, TO><<<grid, 256, 0, s>>>(
+                    R, (const int32_t*)cs, m, n, failed, (TO*)out)));
+  }
+  return check_launch("checksum_recover");
+}
+
+}  // extern "C"

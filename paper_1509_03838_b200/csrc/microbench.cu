@@ -1,0 +1,110 @@
+// microbench.cu -- measured peaks of the MAC flavours (roofline denominators).
+//
+// MEASURED_PEAKS.json has HBM and bf16 only; the conv kernel is bound by the
+// integer / FP64 pipes, so its denominators are measured here on the same box:
+// 16 independent accumulators per thread keep the pipe saturated and the count
+// of issued MACs exact.
+#include "common.cuh"
+
+namespace nent {
+
+constexpr int MB_CHAINS = 16;
+
+__device__ __forceinline__ long long mad_wide_s32(int a, int b, long long c) {
+  long long d;
+  asm volatile("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
+// Every iteration draws one pseudo-random multiplicand x (an LCG step, one
+// extra IMAD shared by the 16 MACs, so the product can be neither hoisted nor
+// strength-reduced) and feeds 16 independent accumulators acc[c] += x * g[c],
+// the exact operand pattern of the convolution's inner loop.
+template <int FLAV>
+__global__ void __launch_bounds__(256) microbench_kernel(int iters, unsigned long long* sink, int k) {
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t x = tid * 2654435761u + (uint32_t)k;
+  int32_t g[MB_CHAINS];
+#pragma unroll
+  for (int c = 0; c < MB_CHAINS; ++c) g[c] = (int32_t)(tid ^ (c * 0x9e37u)) | 1;
+  unsigned long long s = 0;
+  if (FLAV == NENT_MAC_I32) {
+    uint32_t a[MB_CHAINS] = {};
+    for (int it = 0; it < iters; ++it) {
+      x = x * 1664525u + 1013904223u;
+#pragma unroll
+      for (int c = 0; c < MB_CHAINS; ++c) a[c] += x * (uint32_t)g[c];
+    }
+#pragma unroll
+    for (int c = 0; c < MB_CHAINS; ++c) s ^= a[c];
+  } else if (FLAV == NENT_MAC_W64) {
+    long long a[MB_CHAINS] = {};
+    for (int it = 0; it < iters; ++it) {
+      x = x * 1664525u + 1013904223u;
+#pragma unroll
+      for (int c = 0; c < MB_CHAINS; ++c) a[c] = mad_wide_s32((int)x, g[c], a[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < MB_CHAINS; ++c) s ^= (unsigned long long)a[c];
+  } else if (FLAV == NENT_MAC_S64) {
+    long long lo[MB_CHAINS] = {};
+    uint32_t hi[MB_CHAINS] = {};
+    for (int it = 0; it < iters; ++it) {
+      x = x * 1664525u + 1013904223u;
+      const uint32_t xh = x >> 7;
+#pragma unroll
+      for (int c = 0; c < MB_CHAINS; ++c) {
+        lo[c] = mad_wide_s32((int)x, g[c], lo[c]);  // IMAD.WIDE on the low word
+        hi[c] += xh * (uint32_t)g[c];               // IMAD on the high word
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < MB_CHAINS; ++c) s ^= (unsigned long long)lo[c] ^ hi[c];
+  } else if (FLAV == NENT_MAC_F64) {
+    double a[MB_CHAINS] = {};
+    double xd = (double)(tid & 1023);
+    for (int it = 0; it < iters; ++it) {
+      xd = fma(xd, 0.999999, 1.0);
+#pragma unroll
+      for (int c = 0; c < MB_CHAINS; ++c) a[c] = fma(xd, (double)g[c], a[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < MB_CHAINS; ++c) s ^= (unsigned long long)__double_as_longlong(a[c]);
+  } else {
+    unsigned long long a[MB_CHAINS] = {};
+    unsigned long long X = ((unsigned long long)tid << 32) | x;
+    for (int it = 0; it < iters; ++it) {
+      X = X * 6364136223846793005ull + 1442695040888963407ull;
+#pragma unroll
+      for (int c = 0; c < MB_CHAINS; ++c) a[c] += X * (unsigned long long)(long long)g[c];
+    }
+#pragma unroll
+    for (int c = 0; c < MB_CHAINS; ++c) s ^= a[c];
+  }
+  if (s == (unsigned long long)k * 0x9e3779b97f4a7c15ull) sink[tid & 1023] = s;
+}
+
+}  // namespace nent
+
+using namespace nent;
+
+extern "C" int nent_microbench(int kind, int blocks, int threads, int iters,
+                               unsigned long long* sink_dev, double* macs_out, void* stream) {
+  if (blocks < 1 || threads < 32 || threads > 256 || iters < 1) {
+    set_error("microbench: bad launch");
+    return NENT_ERR_PARAM;
+  }
+  cudaStream_t s = as_stream(stream);
+  const int k = 3;
+  double per_thread = (double)iters * MB_CHAINS;
+  switch (kind) {
+    case NENT_MAC_I32: microbench_kernel<NENT_MAC_I32><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
+    case NENT_MAC_W64: microbench_kernel<NENT_MAC_W64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
+    case NENT_MAC_S64: microbench_kernel<NENT_MAC_S64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
+    case NENT_MAC_F64: microbench_kernel<NENT_MAC_F64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
+    case NENT_MAC_G64: microbench_kernel<NENT_MAC_G64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
+    default: set_error("microbench: unknown kind %d", kind); return NENT_ERR_PARAM;
+  }
+  if (macs_out) *macs_out = per_thread * (double)blocks * (double)threads;
+  return check_launch("microbench");
+}

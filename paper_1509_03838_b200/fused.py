@@ -1,0 +1,179 @@
+"""Fused single-pass hot path: entangle -> LSB op -> extract in one kernel.
+
+These are the B200 forms of the reference's composed calls
+``disentangle(apply_entangled(op, entangle(block)), failed)``
+(bench.py:103-106, pipeline.py:97-103) for the op kinds the BASELINE configs
+use, producing bit-identical results:
+
+* ``entangled_conv``       full or circular convolution (cfg1, cfg2, cfg3)
+* ``entangled_chain_conv`` scale -> add -> permute -> full conv (cfg5)
+* ``entangled_inner``      batched inner products (cfg4)
+* ``entangled_outer``      outer products, streamed tile by tile (cfg4)
+* ``plain_conv``           the non-entangled convolution the overhead is
+                           measured against (apply_conventional, ops.py:241-247)
+
+One CTA owns all m streams of an output tile, so entanglement happens while
+the tile is staged into shared memory and extraction happens in registers:
+the entangled words never touch HBM.  ``failed=r`` recovers from the m-1
+other accumulators (worker r's result is computed and discarded, as a failed
+worker's would be); ``failed=None`` pivots on stream 0 and, with
+``verify=True``, checks the redundant stream against the recovered outputs
+(a silent-data-corruption detector the entanglement gives for free).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import MAC_G64, MAC_NAMES, MAC_W64, MAC_X128
+from .blocks import StreamBlock
+from .errors import DeviceError, ParameterError
+from .params import CodecParams
+
+
+@dataclass
+class FusedResult:
+    outputs: StreamBlock
+    flavor: str
+    mismatches: int | None = None  # redundant-stream inconsistencies (failed=None, verify)
+
+
+def _eps_bound(max_c: int, p: CodecParams) -> int:
+    return max_c * ((1 << p.l) + 1)
+
+
+def conv_flavor(max_x: int, g: np.ndarray) -> int:
+    g = np.asarray(g, dtype=np.int64)
+    return D.pick_flavor(max_x, int(np.abs(g.astype(object)).sum()), D.host_max_abs(g))
+
+
+def _prep(block: StreamBlock, dtype=None) -> tuple[torch.Tensor, bool]:
+    host = not block.on_device
+    return D.as_device(block.data, dtype), host
+
+
+def _finish(p, d: torch.Tensor, host: bool) -> StreamBlock:
+    return StreamBlock(p, d.cpu().numpy() if host else d)
+
+
+def entangled_conv(block: StreamBlock, g, failed: int | None = None, mode: str = "full",
+                   verify: bool = True, flavor: int | None = None, out_dtype=torch.int64,
+                   max_c: int | None = None, g_dev: torch.Tensor | None = None,
+                   out: torch.Tensor | None = None, mismatch: torch.Tensor | None = None
+                   ) -> FusedResult:
+    """Recovered conv outputs of every stream in one fused kernel.
+
+    mode="full": linear convolution, n + K - 1 outputs (the reference's
+    circular convolution of the zero-padded stream);
+    mode="circular": the reference's CIRCULAR_CONVOLUTION on n samples."""
+    p = block.params
+    if not 3 <= p.m <= 8:
+        raise ParameterError("the fused kernel holds m in 3..8 streams per tile; "
+                             "use entangle/apply_entangled/disentangle for larger m")
+    c, host = _prep(block)
+    m, n = c.shape
+    g = np.asarray(g, dtype=np.int64) if not isinstance(g, torch.Tensor) else g
+    K = int(g.shape[0])
+    if not 1 <= K <= n and mode == "circular":
+        raise ParameterError(f"kernel length {K} not in 1..{n}")
+    period = n + K - 1 if mode == "full" else n
+    if flavor is None:
+        mc = max_c if max_c is not None else (D.host_max_abs(block.data) if host else D.max_abs(c))
+        flavor = conv_flavor(_eps_bound(mc, p), g if not isinstance(g, torch.Tensor) else g.cpu().numpy())
+    if flavor in (MAC_G64, MAC_X128):
+        raise ParameterError("operands too wide for the fused kernel; use the staged API")
+    if g_dev is None:
+        g_dev = D.taps_tensor(g if not isinstance(g, torch.Tensor) else g.cpu().numpy(), flavor)
+    if verify and failed is None and mismatch is None:
+        mismatch = torch.zeros(1, dtype=torch.int64, device=c.device)
+    d = D.fused_conv(c, g_dev, K, p.l, flavor, failed, p.w > 32, period, n_in=n,
+                     out_dtype=out_dtype, out=out, mismatch=mismatch if failed is None else None)
+    mm = int(mismatch.item()) if (verify and failed is None) else None
+    return FusedResult(_finish(p, d, host), MAC_NAMES[flavor], mm)
+
+
+def plain_conv(block: StreamBlock, g, mode: str = "full", flavor: int | None = None,
+               out_dtype=torch.int64, max_c: int | None = None,
+               g_dev: torch.Tensor | None = None, out: torch.Tensor | None = None) -> FusedResult:
+    """The failure-intolerant convolution of the plain streams (same kernel family)."""
+    p = block.params
+    c, host = _prep(block)
+    m, n = c.shape
+    K = int(len(g))
+    period = n + K - 1 if mode == "full" else n
+    g = np.asarray(g, dtype=np.int64) if not isinstance(g, torch.Tensor) else g.cpu().numpy()
+    if flavor is None:
+        mc = max_c if max_c is not None else (D.host_max_abs(block.data) if host else D.max_abs(c))
+        flavor = conv_flavor(mc, g)
+    if g_dev is None:
+        g_dev = D.taps_tensor(g, flavor)
+    y, ovf = D.conv(c, g_dev, K, flavor, period=period, n_out=period, out_dtype=out_dtype, out=out)
+    if ovf:
+        raise OverflowError(f"{ovf} convolution outputs do not fit int64")
+    return FusedResult(_finish(p, y, host), MAC_NAMES[flavor])
+
+
+def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: int | None = None,
+                         verify: bool = True, flavor: int | None = None, out_dtype=torch.int64
+                         ) -> FusedResult:
+    """cfg5 chain SCALE s -> ELEMENTWISE_ADD a -> PERMUTATION -> full conv, fused.
+
+    The add kernel is self-entangled first (ops.py:250-262) on the device."""
+    p = block.params
+    c, host = _prep(block)
+    m, n = c.shape
+    add_dev = D.as_device(np.asarray(add, dtype=np.int64) if not isinstance(add, torch.Tensor) else add)
+    add_ent = D.shift_add(add_dev, add_dev, p.l)
+    perm_dev = D.as_device(np.asarray(perm, dtype=np.int64) if not isinstance(perm, torch.Tensor) else perm)
+    g = np.asarray(g, dtype=np.int64)
+    K = len(g)
+    if flavor is None:
+        mc = D.host_max_abs(block.data) if host else D.max_abs(c)
+        amax = D.max_abs(add_ent.reshape(1, -1))
+        x_bound = _eps_bound(mc, p) * abs(int(scale)) + amax
+        flavor = conv_flavor(x_bound, g)
+    g_dev = D.taps_tensor(g, flavor)
+    mismatch = torch.zeros(1, dtype=torch.int64, device=c.device) if (verify and failed is None) else None
+    d = D.fused_conv(c, g_dev, K, p.l, flavor, failed, p.w > 32, n + K - 1, n_in=n,
+                     scale=scale, add=add_ent, perm=perm_dev, out_dtype=out_dtype,
+                     mismatch=mismatch)
+    mm = int(mismatch.item()) if mismatch is not None else None
+    return FusedResult(_finish(p, d, host), MAC_NAMES[flavor], mm)
+
+
+def entangled_inner(params: CodecParams, c, g, failed: int | None = None, verify: bool = True,
+                    out_dtype=torch.int64) -> FusedResult:
+    """cfg4: c (m, batch, n) vectors, g (n,) -> recovered dots (m, batch)."""
+    host = not isinstance(c, torch.Tensor)
+    cd = D.as_device(c, None) if not host else torch.from_numpy(
+        np.ascontiguousarray(c, dtype=np.int64)).to(D.device())
+    if cd.dim() != 3 or cd.shape[0] != params.m:
+        raise ParameterError("entangled_inner needs c of shape (m, batch, n)")
+    g = np.asarray(g, dtype=np.int64)
+    mc = D.max_abs(cd.reshape(params.m, -1))
+    eb = _eps_bound(mc, params)
+    flavor = MAC_W64 if (eb < 1 << 31 and D.host_max_abs(g) < 1 << 31) else MAC_G64
+    g_dev = D.taps_tensor(g, flavor)
+    mismatch = torch.zeros(1, dtype=torch.int64, device=cd.device) if (verify and failed is None) else None
+    d = D.fused_inner(cd, g_dev, params.l, failed, params.w > 32, flavor, out_dtype, mismatch)
+    mm = int(mismatch.item()) if mismatch is not None else None
+    return FusedResult(_finish(params, d, host), MAC_NAMES[flavor], mm)
+
+
+def entangled_outer(params: CodecParams, c, g, failed: int | None = None,
+                    out: torch.Tensor | None = None, sums: torch.Tensor | None = None):
+    """cfg4 outer products: d[i, b, u, v] = c[i, b, u] * g[v] through the
+    entangled domain.  Writes ``out`` (m, batch, n, p) when given and adds
+    per-(stream, vector) sums into ``sums`` (m, batch) when given."""
+    cd = c if isinstance(c, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(c, dtype=np.int64)).to(D.device())
+    g_dev = D.taps_tensor(np.asarray(g, dtype=np.int64) if not isinstance(g, torch.Tensor) else g.cpu().numpy())
+    D.fused_outer(cd, g_dev, params.l, failed, params.w > 32, out, sums)
+    return out, sums
+
+
+_ = DeviceError

@@ -1,0 +1,92 @@
+"""Host-buffer path of the fused hot path: pinned host in, pinned host out.
+
+This is what a caller holding plain host arrays goes through (the e2e number
+of bench.py): the signal is cut into output chunks, each chunk's input slice
+(+ K-1 halo) is copied host->device, convolved by the fused
+entangle->conv->extract kernel, and copied back, round-robin over three CUDA
+streams so the H2D copy of chunk i+1, the kernel of chunk i and the D2H copy
+of chunk i-1 overlap (the two copy engines and the SMs run concurrently).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as D
+from .errors import ParameterError
+from .params import CodecParams
+
+
+class ChunkedEntangledConv:
+    """Reusable pipeline for one geometry: m streams of n samples, K taps.
+
+    Inputs/outputs are pinned host tensors (int32 or int64); outputs are the
+    recovered full-convolution samples, n + K - 1 per stream."""
+
+    def __init__(self, params: CodecParams, n: int, g, flavor: int, chunk: int = 1 << 22,
+                 in_dtype=torch.int32, out_dtype=torch.int32, nstreams: int = 3,
+                 device: torch.device | None = None):
+        self.p = params
+        self.n = n
+        self.g = np.asarray(g, dtype=np.int64)
+        self.K = len(self.g)
+        self.L = n + self.K - 1
+        self.flavor = flavor
+        self.chunk = min(chunk, self.L)
+        self.in_dtype, self.out_dtype = in_dtype, out_dtype
+        self.dev = device or D.device()
+        self.g_dev = D.taps_tensor(self.g, flavor)
+        m, H = params.m, self.K - 1
+        self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(nstreams)]
+        self.xbuf = [torch.empty((m, self.chunk + H), dtype=in_dtype, device=self.dev)
+                     for _ in range(nstreams)]
+        self.ybuf = [torch.empty((m, self.chunk), dtype=out_dtype, device=self.dev)
+                     for _ in range(nstreams)]
+        self.launches = 0
+
+    def chunks(self):
+        for s in range(0, self.L, self.chunk):
+            yield s, min(s + self.chunk, self.L)
+
+    def h2d_bytes(self) -> int:
+        es = torch.tensor([], dtype=self.in_dtype).element_size()
+        return self.p.m * self.n * es  # every input sample crosses once (halo re-reads aside)
+
+    def d2h_bytes(self) -> int:
+        es = torch.tensor([], dtype=self.out_dtype).element_size()
+        return self.p.m * self.L * es
+
+    def run(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None) -> int:
+        """Enqueue the whole job; returns the number of kernels launched.
+        The caller synchronises (the last stream's work completes last)."""
+        if not c_host.is_pinned() or not d_host.is_pinned():
+            raise ParameterError("host buffers must be pinned (torch.empty(..., pin_memory=True))")
+        m, H, n = self.p.m, self.K - 1, self.n
+        launches = 0
+        for idx, (s, e) in enumerate(self.chunks()):
+            k = idx % len(self.streams)
+            st = self.streams[k]
+            xb, yb = self.xbuf[k], self.ybuf[k]
+            lo, hi = s - H, e  # input window [lo, hi) of this chunk
+            a, b = max(lo, 0), min(hi, n)
+            width = hi - lo
+            with torch.cuda.stream(st):
+                # recycle buffer k only after its previous D2H finished
+                if lo < 0 or hi > n:
+                    xb[:, :width].zero_()
+                if b > a:
+                    for i in range(m):
+                        xb[i, a - lo:b - lo].copy_(c_host[i, a:b], non_blocking=True)
+                D.fused_conv(xb[:, :width], self.g_dev, self.K, self.p.l, self.flavor, failed,
+                             self.p.w > 32, period=width, n_in=width, y_begin=H, n_out=e - s,
+                             out=yb[:, : e - s])
+                launches += 1
+                for i in range(m):
+                    d_host[i, s:e].copy_(yb[i, : e - s], non_blocking=True)
+        self.launches = launches
+        return launches
+
+    def synchronize(self):
+        for st in self.streams:
+            st.synchronize()

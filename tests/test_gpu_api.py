@@ -1,0 +1,256 @@
+"""Drop-in API parity on the B200: every reference entry point, against the
+fixtures the reference itself produced (tests/golden/make_golden.py).
+
+These tests restate the reference's own test strategy (pkg/tests/test_codec.py,
+test_ops.py, test_pipeline.py) on the sm_100a implementation.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1509_03838_b200 as nent
+from paper_1509_03838_b200 import _lib
+from paper_1509_03838_b200.ops import _apply_raw
+
+pytestmark = pytest.mark.gpu
+
+P3 = nent.CodecParams(3, 32, 11, 10)
+
+
+def test_library_loaded_on_device():
+    L = _lib.lib()
+    assert L.nent_device_ok() == 1
+    assert L.nent_abi_version() == 1
+
+
+# ---- reference golden vectors (test_codec.py / test_ops.py) -----------------
+
+def test_entangle_examples():
+    e = nent.entangle(nent.StreamBlock(P3, [[1], [2], [3]]))
+    assert e.data.ravel().tolist() == [1 + 3 * 2048, 2 + 1 * 2048, 3 + 2 * 2048]
+    e = nent.entangle(nent.StreamBlock(P3, [[-1], [0], [5]]))
+    assert e.data.ravel().tolist() == [10239, -2048, 5]
+    assert not nent.entangle(nent.StreamBlock(P3, np.zeros((3, 5)))).data.any()
+
+
+def test_range_error_fields():
+    bad = nent.input_range(P3).hi + 1
+    with pytest.raises(nent.RangeError) as exc:
+        nent.entangle(nent.StreamBlock(P3, [[0], [bad], [0]]))
+    assert exc.value.stream == 1 and exc.value.value == bad
+
+
+def test_range_first_offender_fixture(golden):
+    p = nent.derive_params(4, 32)
+    with pytest.raises(nent.RangeError) as exc:
+        nent.entangle(nent.StreamBlock(p, golden["range_c"]))
+    e = exc.value
+    assert [e.stream, e.position, e.value, e.bound] == golden["range_expect"].tolist()
+
+
+def test_roundtrip_examples_and_poison():
+    e = nent.entangle(nent.StreamBlock(P3, [[1], [2], [3]]))
+    for r in (0, 1, 2, None):
+        assert nent.disentangle(e, failed=r).data.ravel().tolist() == [1, 2, 3]
+    e.data[0] = nent.word_range(32).hi
+    assert nent.disentangle(e, failed=0).data.ravel().tolist() == [1, 2, 3]
+
+
+def test_entangled_add_example():
+    op = nent.LsbOp(nent.OpKind.ELEMENTWISE_ADD, nent.Kernel.of_vector([5]))
+    delta = nent.apply_entangled(op, nent.entangle(nent.StreamBlock(P3, [[1], [2], [3]])))
+    assert delta.data.ravel().tolist() == [6145 + 10245, 2050 + 10245, 4099 + 10245]
+    for r in (0, 1, 2):
+        assert nent.disentangle(delta, failed=r).data.ravel().tolist() == [6, 7, 8]
+
+
+def test_conv_and_inner_examples():
+    op = nent.LsbOp(nent.OpKind.CIRCULAR_CONVOLUTION, nent.Kernel.of_vector([1, 2, 3, 0]))
+    out = nent.apply_conventional(op, nent.StreamBlock(P3, np.tile([1, 0, 0, 0], (3, 1))))
+    assert out.data.tolist() == [[1, 2, 3, 0]] * 3
+    op = nent.LsbOp(nent.OpKind.INNER_PRODUCT, nent.Kernel.of_vector([4, 5, 6]))
+    out = nent.apply_conventional(op, nent.StreamBlock(P3, np.tile([1, 2, 3], (3, 1))))
+    assert out.data.shape == (3, 1) and out.data.ravel().tolist() == [32, 32, 32]
+
+
+def test_parameter_errors():
+    with pytest.raises(nent.ParameterError):
+        nent.disentangle(nent.entangle(nent.StreamBlock(P3, [[1], [2], [3]])), failed=3)
+    with pytest.raises(nent.ParameterError):
+        nent.disentangle_m3(nent.entangle(nent.StreamBlock(nent.derive_params(4, 32),
+                                                           np.zeros((4, 2)))), failed=0)
+    with pytest.raises(nent.ParameterError):
+        nent.Kernel.of_permutation([0, 0, 1])
+    op = nent.LsbOp(nent.OpKind.INNER_PRODUCT, nent.Kernel.of_vector([1, 2]))
+    with pytest.raises(nent.ParameterError):
+        nent.apply_conventional(op, nent.StreamBlock(P3, np.zeros((3, 4))))
+
+
+# ---- fixtures from the reference -------------------------------------------
+
+def test_codec_fixtures_host_and_device(golden, golden_index):
+    for case in golden_index:
+        key = case["key"]
+        if not key.startswith("codec_"):
+            continue
+        p = nent.CodecParams(case["m"], case["w"], case["l"], case["k"])
+        c = golden[key + "_c"]
+        ent = nent.entangle(nent.StreamBlock(p, c))
+        assert np.array_equal(ent.data, golden[key + "_eps"]), key
+        for r in list(range(p.m)) + [None]:
+            assert np.array_equal(nent.disentangle(ent, failed=r).data, c), (key, r)
+        # device-resident blocks (int64 and, where it fits, int32 sources)
+        dtypes = [torch.int64] + ([torch.int32] if p.w <= 32 else [])
+        for dt in dtypes:
+            dev = torch.from_numpy(c).cuda().to(dt)
+            ent_d = nent.entangle(nent.StreamBlock(p, dev))
+            assert ent_d.on_device
+            assert np.array_equal(ent_d.data.cpu().numpy(), golden[key + "_eps"]), (key, dt)
+            for r in (0, p.m - 1, None):
+                rec = nent.disentangle(ent_d, failed=r)
+                assert np.array_equal(rec.data.cpu().numpy(), c), (key, dt, r)
+
+
+def test_inconsistent_input_fixtures(golden, golden_index):
+    for case in golden_index:
+        if not case.get("garbage"):
+            continue
+        key = case["key"]
+        p = nent.CodecParams(case["m"], case["w"], case["l"], case["k"])
+        delta = golden[key + "_delta"]
+        for r in range(p.m):
+            got = nent.disentangle(nent.EntangledBlock(p, delta), failed=r).data
+            assert np.array_equal(got, golden[f"{key}_r{r}"]), (key, r)
+
+
+def test_m3_fixtures(golden, golden_index):
+    for case in golden_index:
+        if not case.get("m3"):
+            continue
+        key = case["key"]
+        p = nent.CodecParams(3, case["w"], case["l"], case["k"])
+        ent = nent.EntangledBlock(p, golden[key + "_eps"])
+        for r in range(3):
+            assert np.array_equal(nent.disentangle_m3(ent, failed=r).data, golden[f"{key}_r{r}"])
+            assert np.array_equal(nent.disentangle(ent, failed=r).data, golden[f"{key}_r{r}"])
+
+
+def _op(golden, key, kind):
+    K = nent.Kernel
+    ok = nent.OpKind(kind)
+    if ok in (nent.OpKind.PERMUTATION,):
+        return nent.LsbOp(ok, K.of_permutation(golden[key + "_k_perm"]))
+    if ok is nent.OpKind.ROW_GEMM:
+        return nent.LsbOp(ok, K.of_matrix(golden[key + "_k_matrix"]))
+    if ok is nent.OpKind.SCALE:
+        return nent.LsbOp(ok, K.of_scalar(int(golden[key + "_k_scalar"][0])))
+    return nent.LsbOp(ok, K.of_vector(golden[key + "_k_vector"]))
+
+
+def test_op_fixtures_all_kinds(golden, golden_index):
+    n = 0
+    for case in golden_index:
+        if "kind" not in case:
+            continue
+        key = case["key"]
+        p = nent.CodecParams(case["m"], case["w"], case["l"], case["k"])
+        op = _op(golden, key, case["kind"])
+        block = nent.StreamBlock(p, golden[key + "_c"])
+        assert np.array_equal(nent.apply_conventional(op, block).data, golden[key + "_plain"]), key
+        ent = nent.entangle(block)
+        assert np.array_equal(ent.data, golden[key + "_eps"]), key
+        delta = nent.apply_entangled(op, ent)
+        assert np.array_equal(delta.data, golden[key + "_delta"]), key
+        for r in list(range(p.m)) + [None]:
+            rep = nent.run_pipeline(op, block, nent.FailureSpec(nent.Scheme.ENTANGLED, fixed=r))
+            assert rep.recovered
+            assert np.array_equal(rep.outputs.data, golden[key + "_plain"]), (key, r)
+        n += 1
+    assert n == 63
+
+
+@pytest.mark.parametrize("scheme", list(nent.Scheme))
+@pytest.mark.parametrize("m", (3, 8))
+def test_sweep_failures_schemes(golden, scheme, m):
+    key = f"op_conv_m{m}_w32"
+    p = nent.derive_params(m, 32)
+    op = _op(golden, key, "conv")
+    block = nent.StreamBlock(p, golden[key + "_c"])
+    reports = nent.sweep_failures(op, block, scheme)
+    workers = m + 1 if scheme is nent.Scheme.CHECKSUM else m
+    assert len(reports) == workers + 1
+    for rep in reports:
+        if rep.recovered:
+            assert np.array_equal(rep.outputs.data, golden[key + "_plain"])
+        else:
+            alive = [i for i in range(m) if i != rep.failed_worker]
+            assert np.array_equal(rep.outputs.data[alive], golden[key + "_plain"][alive])
+
+
+def test_checksum_all_kinds(golden, golden_index):
+    for case in golden_index:
+        if "kind" not in case or case["w"] != 32 or case["m"] != 3:
+            continue
+        key = case["key"]
+        p = nent.derive_params(3, 32)
+        op = _op(golden, key, case["kind"])
+        block = nent.StreamBlock(p, golden[key + "_c"])
+        coded = nent.checksum_apply(op, nent.checksum_encode(block))
+        for r in [0, 1, 2, 3, None]:
+            damaged = nent.ChecksumBlock(p, coded.data.copy())
+            if r is not None:
+                damaged.data[r] = -(1 << 40)
+            got = nent.checksum_recover(damaged, failed=r).data
+            assert np.array_equal(got, golden[key + "_plain"]), (key, r)
+
+
+def test_no_self_entanglement_breaks(golden):
+    raw = _apply_raw(nent.OpKind.ELEMENTWISE_ADD, nent.Kernel.of_vector(np.full(16, 5)),
+                     nent.entangle(nent.StreamBlock(P3, golden["noselfent_c"])).data)
+    assert np.array_equal(raw, golden["noselfent_delta"])
+    for r in range(3):
+        got = nent.disentangle(nent.EntangledBlock(P3, raw), failed=r).data
+        assert np.array_equal(got, golden[f"noselfent_r{r}"])
+
+
+def test_wide_exact_path_and_overflow(golden):
+    p64 = nent.derive_params(3, 64)
+    op = nent.LsbOp(nent.OpKind.CIRCULAR_CONVOLUTION, nent.Kernel.of_vector([3, -2, 5]))
+    out = nent.apply_conventional(op, nent.StreamBlock(p64, golden["wide_c"])).data
+    assert np.array_equal(out, golden["wide_out"])
+    with pytest.raises(OverflowError):
+        _apply_raw(nent.OpKind.CIRCULAR_CONVOLUTION, nent.Kernel.of_vector([4, 4]),
+                   golden["overflow_big"])
+
+
+def test_inplace_variants():
+    p = nent.derive_params(5, 32)
+    hi = nent.input_range(p).hi
+    c = np.random.default_rng(9).integers(-hi, hi + 1, (5, 256))
+    block = nent.StreamBlock(p, c)
+    ent = nent.entangle(block)
+    block2 = block.copy()
+    ent2 = nent.entangle_inplace(block2)
+    assert np.array_equal(ent.data, ent2.data) and ent2.data is block2.data
+    rec2 = nent.disentangle_inplace(ent2, failed=2)
+    assert np.array_equal(rec2.data, c)
+
+
+def test_counters_closed_forms(golden):
+    for m in (3, 4, 5, 8):
+        key = f"op_conv_m{m}_w32"
+        p = nent.derive_params(m, 32)
+        op = _op(golden, key, "conv")
+        block = nent.StreamBlock(p, golden[key + "_c"])
+        rep = nent.run_pipeline(op, block, nent.FailureSpec(nent.Scheme.ENTANGLED, fixed=0))
+        c = rep.counters
+        assert c.encode_ops + c.decode_ops == (3 * m - 3) * 64
+        assert c.shift_ops > 0 and c.total == c.encode_ops + c.op_ops + c.decode_ops
+
+
+def test_admission_error():
+    op = nent.LsbOp(nent.OpKind.CIRCULAR_CONVOLUTION, nent.Kernel.of_vector(np.full(4, 10**6)))
+    with pytest.raises(nent.AdmissionError):
+        nent.run_pipeline(op, nent.StreamBlock(P3, np.full((3, 4), 1000)),
+                          nent.FailureSpec(nent.Scheme.ENTANGLED))

@@ -1,0 +1,232 @@
+"""Kernel-level parity on the B200 against the CPU oracle, through the C ABI:
+every MAC flavour, the fused entangle->conv->extract kernel for every failure
+index, halo-split output windows, the cfg5 chain, cfg4 inner/outer, and the
+edge cases (n=1, K=1, K=n, ragged tiles, int32/int64 operands)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1509_03838_b200 as nent
+from paper_1509_03838_b200 import _device as D
+from paper_1509_03838_b200 import fused
+from paper_1509_03838_b200._lib import MAC_F64, MAC_G64, MAC_I32, MAC_S64, MAC_W64, MAC_X128
+
+pytestmark = pytest.mark.gpu
+
+
+def rand(seed, shape, lo, hi):
+    return np.random.default_rng(seed).integers(lo, hi + 1, shape, dtype=np.int64)
+
+
+def exact_flavors(max_x, g):
+    """Every flavour that is exact for these operands."""
+    g = np.asarray(g, dtype=np.int64)
+    sg = int(np.abs(g).sum())
+    mg = int(np.abs(g).max())
+    b = max_x * max(sg, 1)
+    out = [MAC_G64, MAC_X128]
+    if b < 1 << 31:
+        out.append(MAC_I32)
+    if b < 1 << 53:
+        out.append(MAC_F64)
+    if max_x < 1 << 31 and mg < 1 << 31:
+        out.append(MAC_W64)
+    if mg < 1 << 31:
+        out.append(MAC_S64)
+    return out
+
+
+@pytest.mark.parametrize("n,K", [(1, 1), (5, 1), (7, 7), (100, 33), (1537, 64), (5000, 256),
+                                 (3000, 1000), (20000, 2049), (4096, 4096)])
+def test_conv_all_flavors_circular_and_full(oracle, n, K):
+    x = rand(n * 7 + K, (3, n), -(1 << 20), 1 << 20)
+    g = rand(K, (K,), -300, 300)
+    ref_circ = oracle.circ_conv(x, g)
+    ref_full = oracle.full_conv(x, g)
+    xd = torch.from_numpy(x).cuda()
+    for flavor in exact_flavors(1 << 20, g):
+        gd = D.taps_tensor(g, flavor)
+        y, _ = D.conv(xd, gd, K, flavor)
+        assert np.array_equal(y.cpu().numpy(), ref_circ), (flavor, n, K)
+        y, _ = D.conv(xd, gd, K, flavor, period=n + K - 1)
+        assert np.array_equal(y.cpu().numpy(), ref_full), (flavor, n, K)
+
+
+@pytest.mark.parametrize("rows", [1, 2, 3, 4, 5, 8, 11])
+def test_conv_row_groups(oracle, rows):
+    x = rand(rows, (rows, 777), -5000, 5000)
+    g = rand(rows + 1, (40,), -100, 100)
+    ref = oracle.circ_conv(x, g)
+    for flavor in (MAC_I32, MAC_F64, MAC_W64, MAC_S64):
+        y, _ = D.conv(torch.from_numpy(x).cuda(), D.taps_tensor(g, flavor), 40, flavor)
+        assert np.array_equal(y.cpu().numpy(), ref), (rows, flavor)
+
+
+def test_conv_int32_operands_and_outputs(oracle):
+    x = rand(3, (3, 4000), -1000, 1000)
+    g = rand(4, (100,), -100, 100)
+    ref = oracle.full_conv(x, g)
+    xd = torch.from_numpy(x).cuda().to(torch.int32)
+    for flavor in (MAC_I32, MAC_F64, MAC_W64, MAC_S64):
+        for out_dtype in (torch.int32, torch.int64):
+            y, _ = D.conv(xd, D.taps_tensor(g, flavor), 100, flavor, period=4099, out_dtype=out_dtype)
+            assert np.array_equal(y.to(torch.int64).cpu().numpy(), ref), (flavor, out_dtype)
+
+
+def test_conv_wide_operands(oracle):
+    # |x| up to 2^45: S64 (g fits int32) and G64 / X128 are the exact flavours
+    x = rand(11, (2, 3000), -(1 << 45), 1 << 45)
+    g = rand(12, (50,), -1000, 1000)
+    ref = oracle.circ_conv(x, g)
+    for flavor in (MAC_S64, MAC_G64, MAC_X128):
+        y, ovf = D.conv(torch.from_numpy(x).cuda(), D.taps_tensor(g, flavor), 50, flavor)
+        assert ovf == 0
+        assert np.array_equal(y.cpu().numpy(), ref), flavor
+
+
+def test_conv_halo_windows(oracle):
+    """Output windows [y_begin, y_begin+n_out) of the full conv, as the
+    halo-split shards compute them."""
+    x = rand(21, (3, 10000), -2048, 2047)
+    g = rand(22, (256,), -2048, 2047)
+    ref = oracle.full_conv(x, g)
+    xd = torch.from_numpy(x).cuda()
+    L = 10000 + 255
+    for flavor in (MAC_F64, MAC_S64):
+        gd = D.taps_tensor(g, flavor)
+        for y0, cnt in [(0, 1), (0, 300), (255, 5000), (9990, 265), (4321, 1)]:
+            y, _ = D.conv(xd, gd, 256, flavor, period=L, y_begin=y0, n_out=cnt)
+            assert np.array_equal(y.cpu().numpy(), ref[:, y0:y0 + cnt]), (flavor, y0, cnt)
+
+
+@pytest.mark.parametrize("m,w", [(3, 32), (4, 32), (5, 32), (8, 32), (3, 64), (4, 64), (3, 48),
+                                 (6, 64), (7, 64)])
+def test_fused_conv_every_failure(oracle, m, w):
+    p = nent.derive_params(m, w)
+    hi = nent.output_range(p).hi
+    K = 96
+    g = rand(m + w, (K,), -50, 50)
+    bound = max(1, min(hi // int(np.abs(g).sum()), 1 << 20))
+    c = rand(m * w, (m, 2500), -bound, bound)
+    ref = oracle.full_conv(c, g)
+    block = nent.StreamBlock(p, c)
+    eb = bound * ((1 << p.l) + 1)
+    for flavor in [f for f in exact_flavors(eb, g) if f in (MAC_I32, MAC_F64, MAC_W64, MAC_S64)]:
+        for r in [None] + list(range(m)):
+            res = fused.entangled_conv(block, g, failed=r, flavor=flavor)
+            assert np.array_equal(res.outputs.data, ref), (m, w, flavor, r)
+            if r is None:
+                assert res.mismatches == 0
+
+
+def test_fused_conv_circular_mode_and_dtypes(oracle):
+    p = nent.derive_params(3, 32)
+    c = rand(5, (3, 3001), -100, 100)
+    g = rand(6, (64,), -100, 100)
+    ref = oracle.circ_conv(c, g)
+    dev = torch.from_numpy(c).cuda().to(torch.int32)
+    for out_dtype in (torch.int32, torch.int64):
+        res = fused.entangled_conv(nent.StreamBlock(p, dev), g, failed=1, mode="circular",
+                                   out_dtype=out_dtype)
+        assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), ref)
+
+
+def test_fused_detects_inconsistency():
+    """Forcing a too-narrow flavour makes the entangled words wrap; the
+    redundant-stream check then reports it instead of returning garbage silently."""
+    p = nent.derive_params(3, 32)
+    c = rand(7, (3, 4000), -1000, 1000)
+    g = rand(8, (200,), -2000, 2000)
+    res = fused.entangled_conv(nent.StreamBlock(p, c), g, failed=None, flavor=MAC_I32)
+    assert res.mismatches > 0
+
+
+def test_plain_conv_matches_reference(oracle):
+    p = nent.derive_params(3, 64)
+    c = rand(31, (3, 7000), -2048, 2047)
+    g = rand(32, (256,), -2048, 2047)
+    ref = oracle.full_conv(c, g)
+    for flavor in (MAC_I32, MAC_F64, MAC_W64, MAC_S64):
+        res = fused.plain_conv(nent.StreamBlock(p, c), g, flavor=flavor)
+        assert np.array_equal(res.outputs.data, ref), flavor
+
+
+def test_chain_conv_cfg5_shape(oracle):
+    from paper_1509_03838_b200 import workloads
+    wl = workloads.make(5, n=6000)
+    x = (wl.c * wl.scale + wl.add)[:, wl.perm]
+    ref = oracle.full_conv(x, wl.g)
+    for r in [None] + list(range(8)):
+        res = fused.entangled_chain_conv(nent.StreamBlock(wl.params, wl.c), wl.scale, wl.add,
+                                         wl.perm, wl.g, failed=r)
+        assert np.array_equal(res.outputs.data, ref), r
+        if r is None:
+            assert res.mismatches == 0
+
+
+def test_chain_conv_single_stream_worker(oracle):
+    """The stream-per-GPU worker: one entangled stream (a << l) + b, chain, conv."""
+    from paper_1509_03838_b200 import workloads
+    wl = workloads.make(5, n=3000)
+    p = wl.params
+    eps = oracle.entangle(wl.c, p.l)
+    a_ent = oracle.self_entangle("add", wl.add, p.l)
+    x = (eps * wl.scale + a_ent)[:, wl.perm]
+    ref = oracle.full_conv(x, wl.g)
+    c = torch.from_numpy(wl.c).cuda()
+    gd = D.taps_tensor(wl.g, MAC_I32)
+    add = D.shift_add(torch.from_numpy(wl.add).cuda(), torch.from_numpy(wl.add).cuda(), p.l)
+    perm = torch.from_numpy(wl.perm).cuda()
+    for i in range(8):
+        y = D.chain_conv(c[(i - 1) % 8], c[i], gd, wl.K, p.l, MAC_I32, 3000 + wl.K - 1,
+                         scale=wl.scale, add=add, perm=perm)
+        assert np.array_equal(y.cpu().numpy(), ref[i]), i
+
+
+def test_fused_inner_and_staged_inner(oracle):
+    from paper_1509_03838_b200 import workloads
+    wl = workloads.make(4, n=512, batch=300)
+    m, B, n = wl.c.shape
+    ref = oracle.apply_raw("dot", wl.c.reshape(m * B, n), vector=wl.g).reshape(m, B)
+    for r in [None, 0, 1, 2]:
+        res = fused.entangled_inner(wl.params, wl.c, wl.g, failed=r)
+        assert np.array_equal(res.outputs.data, ref), r
+    # staged: reference API per vector
+    blk = nent.StreamBlock(wl.params, wl.c[:, 5, :])
+    op = nent.LsbOp(nent.OpKind.INNER_PRODUCT, nent.Kernel.of_vector(wl.g))
+    rec = nent.disentangle(nent.apply_entangled(op, nent.entangle(blk)), failed=1)
+    assert np.array_equal(rec.data.ravel(), ref[:, 5])
+
+
+def test_fused_outer(oracle):
+    from paper_1509_03838_b200 import workloads
+    wl = workloads.make(4, n=64, batch=5)
+    m, B, n = wl.c.shape
+    g = wl.g[:48]
+    ref = wl.c[:, :, :, None] * g[None, None, None, :]
+    c = torch.from_numpy(wl.c).cuda()
+    for r in [None, 0, 2]:
+        out = torch.empty((m, B, n, len(g)), dtype=torch.int64, device="cuda")
+        sums = torch.zeros((m, B), dtype=torch.int64, device="cuda")
+        fused.entangled_outer(wl.params, c, g, failed=r, out=out, sums=sums)
+        assert np.array_equal(out.cpu().numpy(), ref), r
+        assert np.array_equal(sums.cpu().numpy(), ref.sum(axis=(2, 3))), r
+
+
+def test_extract_int32_and_peer_style_rows(oracle):
+    p = nent.derive_params(4, 32)
+    c = rand(40, (4, 10000), -5000, 5000)
+    eps = oracle.entangle(c, p.l)
+    rows = [torch.from_numpy(eps[i]).cuda().to(torch.int32) for i in range(4)]
+    for r in range(4):
+        rows_r = [None if i == r else rows[i] for i in range(4)]
+        out, _ = D.extract(rows_r, 4, p.l, r, wide=False, out_dtype=torch.int32)
+        assert np.array_equal(out.to(torch.int64).cpu().numpy(), c)
+
+
+@pytest.mark.parametrize("kind", [MAC_I32, MAC_F64, MAC_W64, MAC_S64, MAC_G64])
+def test_microbench_runs(kind):
+    macs = D.microbench(kind, 148, 128, 10)
+    torch.cuda.synchronize()
+    assert macs == 148 * 128 * 10 * 16

@@ -44,7 +44,7 @@ L2_BYTES = 126 * 1024 * 1024
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -67,58 +67,68 @@ def sha(a: np.ndarray) -> str:
 # ----------------------------------------------------------------- clocks --
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons polled through NVML every
+    ~2 ms while the timed region runs (the same counters nvidia-smi's
+    clocks.sm / clocks_event_reasons.* report); nvidia-smi is the fallback."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.index, self.period = index, period_s
+        self.samples: list[tuple[float, int]] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self.source = "nvml"
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            masks = [(nm, getattr(N, attr)) for nm, attr in self.REASONS if hasattr(N, attr)]
+
+            def poll():
+                while not self._stop.is_set():
+                    self.samples.append((time.perf_counter(), N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                    bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for nm, mask in masks:
+                        if bits & mask:
+                            self.reasons.add(nm)
+                    time.sleep(self.period)
+
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            time.sleep(3 * self.period)
+        except Exception as exc:  # NVML unavailable: one nvidia-smi read instead
+            self.source = f"nvidia-smi ({type(exc).__name__})"
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=1)
+        if self.t is None:
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                      "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=10).stdout.split(",")
+                self.samples = [(0.0, int(float(out[0])))]
+                self.max_mhz = int(float(out[1]))
+            except Exception:
+                pass
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [v for _, v in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": self.source,
+                "sm_mhz_min": min(sm) if sm else None}
 
 
 # -------------------------------------------------------------- workload --
@@ -257,7 +267,9 @@ def run_ours(args):
 
     # ---------------- measured MAC-pipe peaks (roofline denominators) ----------------
     peaks = {}
-    for kind in (MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64):
+    names = dict(MAC_NAMES)
+    names[7] = "imma_s8_mma_sync"
+    for kind in (MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64, 7):
         D.microbench(kind, 148 * 4, 256, 64)  # warm
         best = 0.0
         for _ in range(3):
@@ -267,7 +279,7 @@ def run_ours(args):
             b.record(stream)
             torch.cuda.synchronize(dev)
             best = max(best, macs / (a.elapsed_time(b) / 1e3))
-        peaks[MAC_NAMES[kind]] = best
+        peaks[names[kind]] = best
     kern_ms = statistics.median(t_e)  # one fused launch per step, measured on its stream
     macs_launch = m * n * K  # algorithmic MACs per launch (M*N*K)
     achieved_tflops = 2 * macs_launch / (kern_ms / 1e3) / 1e12

@@ -194,8 +194,10 @@ int nent_checksum_recover(const void *const *x, int x_bits, const void *cs, int 
 
 /* ---- measurement ------------------------------------------------------------ */
 
+#define NENT_BENCH_IMMA 7 /* microbenchmark only: mma.sync m16n8k32 s8 (legacy IMMA) */
+
 /* Integer / FP64 pipe microbenchmark used for the roofline denominators.
- * kind: NENT_MAC_* flavour; launches blocks x threads threads each doing
+ * kind: NENT_MAC_* flavour or NENT_BENCH_IMMA; launches blocks x threads threads each doing
  * `iters` x 16 independent MACs; sink_dev receives a value so nothing is
  * dead-code eliminated. Returns MACs issued via *macs_out (host). */
 int nent_microbench(int kind, int blocks, int threads, int iters, unsigned long long *sink_dev,

@@ -199,8 +199,20 @@ __device__ __forceinline__ int64_t conv_prologue(const ConvArgs& A, int row, int
   return e;
 }
 
+// 4 CTAs (16 warps) per SM when the accumulators leave room for <= 128
+// registers per thread, else 2 (<= 255 registers, no spills).
+// (checked with -Xptxas -warn-spills: every instantiation is spill-free)
+__host__ __device__ constexpr int conv_min_blocks(int flav, int ms) {
+  return (flav == NENT_MAC_I32 && (ms <= 3 || pick_R(flav, ms) == 4)) ||
+                 (flav == NENT_MAC_F64 && ms <= 3) || (flav == NENT_MAC_W64 && ms <= 2) ||
+                 (flav == NENT_MAC_S64 && ms == 1)
+             ? 4
+             : 2;
+}
+
 template <int FLAV, int MS, bool EXTRACT>
-__global__ void __launch_bounds__(CV_NT, 2) conv_tile_kernel(const __grid_constant__ ConvArgs A) {
+__global__ void __launch_bounds__(CV_NT, conv_min_blocks(FLAV, MS))
+    conv_tile_kernel(const __grid_constant__ ConvArgs A) {
   using MT = Mac<FLAV>;
   typedef typename MT::XT XT;
   typedef typename MT::GT GT;
@@ -295,12 +307,10 @@ __global__ void __launch_bounds__(CV_NT, 2) conv_tile_kernel(const __grid_consta
       int64_t dl[MS], orot[MS];
 #pragma unroll
       for (int s = 0; s < MS; ++s) dl[s] = MT::value(acc[s][r]);
-      bool ovf = recover_regs<MS>(dl, pivot, A.l, A.wide != 0, orot);
+      recover_regs_valid<MS>(dl, pivot, A.l, orot);
       if (verify) {
         // delta_0 was not used by the recovery: it must equal (d_{m-1} << l) + d_0
-        bad += (ovf || dl[0] != wadd(wshl(orot[MS - 1], A.l), orot[0])) ? 1u : 0u;
-      } else {
-        bad += ovf ? 1u : 0u;
+        bad += (dl[0] != wadd(wshl(orot[MS - 1], A.l), orot[0])) ? 1u : 0u;
       }
 #pragma unroll
       for (int t = 0; t < MS; ++t) {

@@ -163,9 +163,8 @@ fused_inner_kernel(const Rows c, int64_t batch, int64_t n, int l, const TG* __re
       int64_t dl[MT], orot[MT];
 #pragma unroll
       for (int s = 0; s < MT; ++s) dl[s] = (int64_t)acc[s];
-      bool ovf = recover_regs<MT>(dl, pivot, l, wide != 0, orot);
-      if (verify) bad += (ovf || dl[0] != wadd(wshl(orot[MT - 1], l), orot[0])) ? 1u : 0u;
-      else bad += ovf ? 1u : 0u;
+      recover_regs_valid<MT>(dl, pivot, l, orot);
+      if (verify) bad += (dl[0] != wadd(wshl(orot[MT - 1], l), orot[0])) ? 1u : 0u;
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         int row = pivot + t;
@@ -203,7 +202,7 @@ fused_outer_kernel(const Rows c, int64_t n, int l, const TG* __restrict__ g, int
       int64_t dl[MT], orot[MT];
 #pragma unroll
       for (int s = 0; s < MT; ++s) dl[s] = wmul(e[s], gv);
-      recover_regs<MT>(dl, pivot, l, wide != 0, orot);
+      recover_regs_valid<MT>(dl, pivot, l, orot);
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         int row = pivot + t;

@@ -84,6 +84,29 @@ __global__ void __launch_bounds__(256) microbench_kernel(int iters, unsigned lon
   if (s == (unsigned long long)k * 0x9e3779b97f4a7c15ull) sink[tid & 1023] = s;
 }
 
+// Legacy warp-level integer tensor-core MMA (IMMA, mma.sync m16n8k32 s8*s8+s32):
+// 16 independent accumulator fragments per warp; 4096 MACs per instruction.
+__global__ void __launch_bounds__(256) microbench_imma_kernel(int iters, unsigned long long* sink, int k) {
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t a0 = tid * 0x01010101u + k, a1 = a0 ^ 0x5a5a5a5au, a2 = a0 + 0x11111111u, a3 = a0 * 3u;
+  uint32_t b0 = tid ^ 0x3c3c3c3cu, b1 = b0 + (uint32_t)k;
+  int acc[MB_CHAINS][4] = {};
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < MB_CHAINS; ++c)
+      asm volatile(
+          "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+          "{%0,%1,%2,%3};"
+          : "+r"(acc[c][0]), "+r"(acc[c][1]), "+r"(acc[c][2]), "+r"(acc[c][3])
+          : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    a0 += 0x01020304u;
+  }
+  unsigned long long s = 0;
+#pragma unroll
+  for (int c = 0; c < MB_CHAINS; ++c) s ^= (unsigned)(acc[c][0] ^ acc[c][1] ^ acc[c][2] ^ acc[c][3]);
+  if (s == (unsigned long long)k * 0x9e3779b97f4a7c15ull) sink[tid & 1023] = s;
+}
+
 }  // namespace nent
 
 using namespace nent;
@@ -103,6 +126,10 @@ extern "C" int nent_microbench(int kind, int blocks, int threads, int iters,
     case NENT_MAC_S64: microbench_kernel<NENT_MAC_S64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
     case NENT_MAC_F64: microbench_kernel<NENT_MAC_F64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
     case NENT_MAC_G64: microbench_kernel<NENT_MAC_G64><<<blocks, threads, 0, s>>>(iters, sink_dev, k); break;
+    case NENT_BENCH_IMMA:
+      microbench_imma_kernel<<<blocks, threads, 0, s>>>(iters, sink_dev, k);
+      per_thread = (double)iters * MB_CHAINS * (16.0 * 8 * 32 / 32);  // 4096 MACs per warp-MMA
+      break;
     default: set_error("microbench: unknown kind %d", kind); return NENT_ERR_PARAM;
   }
   if (macs_out) *macs_out = per_thread * (double)blocks * (double)threads;

@@ -93,4 +93,38 @@ __device__ __forceinline__ bool recover_regs(const int64_t (&dl)[MT], int r, int
   return recover_rot<MT>(rot, MT, l, wide, orot);
 }
 
+// Recovery for CONSISTENT entangled words (delta_i = (d_{i-1} << l) + d_i with
+// every d fitting its word), as the fused kernels produce from admitted
+// inputs: the low (m-1)l pivot bits are exact under 64-bit wrap-around for any
+// w <= 64, giving d_{r-1}; the rest follow backwards exactly,
+//   d_{j-1} = (delta_j - d_j) >> l,   j = r-1, r-2, ..., r+1,
+// so no 128-bit pivot is needed even for w = 64.  Results equal the
+// reference formula on such input; the fused kernels' redundant-stream check
+// flags any input that is not consistent.
+template <int MT>
+__device__ __forceinline__ void recover_regs_valid(const int64_t (&dl)[MT], int r, int l,
+                                                   int64_t (&orot)[MT]) {
+  int64_t rot[MT];
+#pragma unroll
+  for (int t = 0; t < MT - 1; ++t) {
+    int idx = r + 1 + t;
+    idx -= (idx >= MT) ? MT : 0;
+    idx -= (idx >= MT) ? MT : 0;
+    rot[t] = select_mod<MT>(dl, idx);
+  }
+  const int low = (MT - 1) * l;
+  const uint64_t mask = (((uint64_t)1) << low) - 1;
+  const uint64_t sbit = ((uint64_t)1) << (low - 1);
+  uint64_t acc = (uint64_t)rot[0] << ((MT - 2) * l);
+#pragma unroll
+  for (int t = 1; t < MT - 1; ++t) {
+    const uint64_t term = (uint64_t)rot[t] << ((MT - 2 - t) * l);
+    acc = (t & 1) ? acc - term : acc + term;
+  }
+  const int64_t v = (int64_t)(((acc & mask) ^ sbit) - sbit);
+  orot[MT - 1] = (MT & 1) ? wneg(v) : v;
+#pragma unroll
+  for (int t = MT - 1; t >= 1; --t) orot[t - 1] = wsub(rot[t - 1], orot[t]) >> l;
+}
+
 }  // namespace nent

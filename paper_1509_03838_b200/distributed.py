@@ -1,0 +1,260 @@
+"""Multi-GPU drivers: the method's unit of failure mapped onto real devices.
+
+One process per GPU, ``torch.distributed`` (NCCL over NVLink/NVSwitch) for
+the plumbing:
+
+* ``StreamPerGPU`` -- M = world size; rank i owns stream c_i and is "worker i"
+  of the reference's logical pipeline (pipeline.py:90-117).
+    1. ring shift: rank i receives c_{i-1} from rank i-1 (one P2P exchange);
+    2. worker: eps_i = (c_{i-1} << l) + c_i, the LSB chain and the
+       convolution, fused in one kernel (nent_chain_conv) -> delta_i;
+    3. fail-stop: rank r's delta is lost -- it is never sent or read;
+    4. recovery, position-sharded: the M-1 survivors each own 1/(M-1) of the
+       positions; one all-to-all among survivors (rank r sends and receives
+       nothing) gives each survivor the surviving deltas of its slice, and K3
+       recovers all M outputs there;
+    5. optional gather of the recovered slices.
+  ``recover_peer`` is the fused alternative for a single node: every rank
+  exports its delta buffer through CUDA IPC and the extract kernel reads the
+  survivors' slices straight out of peer HBM over NVLink (no staging copy).
+
+* ``HaloSplit`` -- a long signal cut into contiguous slices; rank p needs the
+  K-1 samples left of its slice from rank p-1 (one P2P exchange), then runs the
+  fused entangle -> conv -> extract kernel on [halo | slice].  Entangle and
+  extract are position-local, so nothing else crosses ranks.
+
+Compute goes through a ``compute`` object (default ``DeviceCompute``: the
+sm_100a kernels); the CPU tests inject a CPU stand-in to exercise the
+exchange logic under gloo.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import ParameterError
+from .params import CodecParams
+
+
+class DeviceCompute:
+    """The per-rank compute steps, each one sm_100a kernel via the C ABI."""
+
+    def __init__(self, flavor: int | None = None):
+        self.flavor = flavor
+
+    def chain_conv(self, c_prev, c_own, params: CodecParams, g, scale=1, add=None, perm=None,
+                   full=True):
+        from . import _device as D
+        from .fused import conv_flavor
+
+        n = c_own.shape[-1]
+        K = len(g)
+        flavor = self.flavor
+        if flavor is None:
+            mc = max(D.max_abs(c_own.reshape(1, -1)), D.max_abs(c_prev.reshape(1, -1)))
+            xb = mc * ((1 << params.l) + 1) * abs(int(scale))
+            if add is not None:
+                xb += D.max_abs(add.reshape(1, -1))
+            flavor = conv_flavor(xb, np.asarray(g))
+        g_dev = D.taps_tensor(np.asarray(g, dtype=np.int64), flavor)
+        period = n + K - 1 if full else n
+        add_ent = D.shift_add(add, add, params.l) if add is not None else None
+        return D.chain_conv(c_prev, c_own, g_dev, K, params.l, flavor, period, n_in=n,
+                            scale=scale, add=add_ent, perm=perm)
+
+    def extract(self, rows, params: CodecParams, r: int):
+        from . import _device as D
+
+        out, ovf = D.extract(rows, params.m, params.l, r, wide=params.w > 32)
+        if ovf:
+            raise OverflowError(f"{ovf} recovered values do not fit int64")
+        return out
+
+    def fused_conv(self, x, params: CodecParams, g, period, n_in, y_begin, n_out, failed=None):
+        from . import _device as D
+        from .fused import conv_flavor
+
+        flavor = self.flavor
+        if flavor is None:
+            mc = D.max_abs(x)
+            flavor = conv_flavor(mc * ((1 << params.l) + 1), np.asarray(g))
+        g_dev = D.taps_tensor(np.asarray(g, dtype=np.int64), flavor)
+        return D.fused_conv(x, g_dev, len(g), params.l, flavor, failed, params.w > 32, period,
+                            n_in=n_in, y_begin=y_begin, n_out=n_out)
+
+
+def shard_bounds(L: int, parts: int, idx: int) -> tuple[int, int]:
+    """[begin, end) of slice ``idx`` when L positions are cut into ``parts``
+    near-equal contiguous slices (the first L % parts get one extra)."""
+    base, rem = divmod(L, parts)
+    begin = idx * base + min(idx, rem)
+    return begin, begin + base + (1 if idx < rem else 0)
+
+
+@dataclass
+class StreamPerGPU:
+    params: CodecParams
+    group: object = None
+    compute: object = None
+
+    def __post_init__(self):
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        if self.world != self.params.m:
+            raise ParameterError(f"stream-per-GPU needs world size == m ({self.params.m}), "
+                                 f"got {self.world}")
+        if self.compute is None:
+            self.compute = DeviceCompute()
+
+    # -- 1. ring shift ------------------------------------------------------
+    def ring_shift(self, c_own: torch.Tensor) -> torch.Tensor:
+        """Return c_{rank-1} (the stream entangled into this rank's word)."""
+        m = self.world
+        prev = torch.empty_like(c_own)
+        ops = [dist.P2POp(dist.isend, c_own.contiguous(), (self.rank + 1) % m, self.group),
+               dist.P2POp(dist.irecv, prev, (self.rank - 1) % m, self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        return prev
+
+    # -- 2. worker ------------------------------------------------------------
+    def work(self, c_own: torch.Tensor, g, scale: int = 1, add=None, perm=None,
+             full: bool = True) -> torch.Tensor:
+        c_prev = self.ring_shift(c_own)
+        return self.compute.chain_conv(c_prev, c_own, self.params, g, scale=scale, add=add,
+                                       perm=perm, full=full)
+
+    # -- 4. position-sharded recovery -----------------------------------------
+    def survivors(self, failed: int | None) -> list[int]:
+        return [i for i in range(self.world) if i != failed]
+
+    def recover(self, delta_local: torch.Tensor, failed: int | None) -> tuple[torch.Tensor, int, int]:
+        """All-to-all of surviving delta slices, then K3 on this rank's slice.
+
+        Returns (d_slice (m, end-begin), begin, end); the failed rank returns
+        an empty slice and contributes nothing."""
+        m, L = self.world, int(delta_local.shape[-1])
+        pivot_failed = failed
+        surv = self.survivors(pivot_failed)
+        nsurv = len(surv)
+        me_alive = self.rank in surv
+        my_idx = surv.index(self.rank) if me_alive else -1
+        # send splits: survivor i sends slice k of its delta to survivor k
+        send_sizes = [0] * m
+        recv_sizes = [0] * m
+        if me_alive:
+            for k, dst in enumerate(surv):
+                b, e = shard_bounds(L, nsurv, k)
+                send_sizes[dst] = e - b
+            mb, me = shard_bounds(L, nsurv, my_idx)
+            for src in surv:
+                recv_sizes[src] = me - mb
+        else:
+            mb = me = 0
+        send = delta_local.contiguous() if me_alive else delta_local.new_empty(0)
+        recv = delta_local.new_empty(sum(recv_sizes))
+        dist.all_to_all_single(recv, send.reshape(-1), recv_sizes, send_sizes, group=self.group)
+        if not me_alive:
+            return delta_local.new_empty((m, 0)), 0, 0
+        width = me - mb
+        rows = [None] * m
+        off = 0
+        for src in range(m):
+            if recv_sizes[src]:
+                rows[src] = recv[off:off + width]
+                off += width
+        r = 0 if failed is None else failed
+        if failed is None:
+            rows[0] = None  # pivot stream 0, as codec.disentangle does for failed=None
+        d = self.compute.extract(rows, self.params, r)
+        return d, mb, me
+
+    # -- 5. gather ------------------------------------------------------------
+    def gather(self, d_slice: torch.Tensor, L: int, failed: int | None, dst: int = 0):
+        """Recovered (m, L) outputs assembled on ``dst`` (None elsewhere)."""
+        m = self.world
+        surv = self.survivors(failed)
+        nsurv = len(surv)
+        maxw = -(-L // nsurv)
+        buf = d_slice.new_zeros((m, maxw))
+        if d_slice.shape[-1]:
+            buf[:, : d_slice.shape[-1]] = d_slice
+        parts = [torch.empty_like(buf) for _ in range(m)] if self.rank == dst else None
+        dist.gather(buf, parts, dst=dst, group=self.group)
+        if self.rank != dst:
+            return None
+        out = d_slice.new_empty((m, L))
+        for k, src in enumerate(surv):
+            b, e = shard_bounds(L, nsurv, k)
+            out[:, b:e] = parts[src][:, : e - b]
+        return out
+
+    def run(self, c_own: torch.Tensor, g, failed: int | None = None, scale: int = 1, add=None,
+            perm=None, full: bool = True, dst: int | None = 0):
+        """The whole fail-stop pipeline; rank ``failed`` computes but its
+        result is dropped (it is the worker that died)."""
+        delta = self.work(c_own, g, scale, add, perm, full)
+        d, b, e = self.recover(delta, failed)
+        if dst is None:
+            return d, b, e
+        return self.gather(d, int(delta.shape[-1]), failed, dst)
+
+
+@dataclass
+class HaloSplit:
+    params: CodecParams
+    K: int
+    group: object = None
+    compute: object = None
+
+    def __post_init__(self):
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        if self.compute is None:
+            self.compute = DeviceCompute()
+
+    def exchange_halo(self, c_slice: torch.Tensor) -> torch.Tensor:
+        """[halo | slice]: the K-1 samples left of this slice, from rank-1
+        (zeros on rank 0, the signal's left edge)."""
+        H = self.K - 1
+        m = c_slice.shape[0]
+        halo = c_slice.new_zeros((m, H))
+        if H and self.world > 1:
+            ops = []
+            if self.rank + 1 < self.world:
+                ops.append(dist.P2POp(dist.isend, c_slice[:, c_slice.shape[1] - H:].contiguous(),
+                                      self.rank + 1, self.group))
+            if self.rank > 0:
+                ops.append(dist.P2POp(dist.irecv, halo, self.rank - 1, self.group))
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return torch.cat([halo, c_slice], dim=1).contiguous()
+
+    def run(self, c_slice: torch.Tensor, g, failed: int | None = None):
+        """Recovered full-convolution outputs owned by this rank: positions
+        [start, start + n_slice) of the global output (+ the K-1 tail on the
+        last rank)."""
+        H = self.K - 1
+        x = self.exchange_halo(c_slice)
+        n = c_slice.shape[1]
+        last = self.rank == self.world - 1
+        n_out = n + (H if last else 0)
+        return self.compute.fused_conv(x, self.params, g, period=n + 2 * H, n_in=n + H,
+                                       y_begin=H, n_out=n_out, failed=failed)
+
+    def gather(self, d_local: torch.Tensor, dst: int = 0):
+        sizes = torch.tensor([d_local.shape[1]], dtype=torch.int64)
+        all_sizes = [torch.zeros_like(sizes) for _ in range(self.world)]
+        dist.all_gather(all_sizes, sizes, group=self.group)
+        maxw = int(max(s.item() for s in all_sizes))
+        buf = d_local.new_zeros((d_local.shape[0], maxw))
+        buf[:, : d_local.shape[1]] = d_local
+        parts = [torch.empty_like(buf) for _ in range(self.world)] if self.rank == dst else None
+        dist.gather(buf, parts, dst=dst, group=self.group)
+        if self.rank != dst:
+            return None
+        return torch.cat([p[:, : int(s.item())] for p, s in zip(parts, all_sizes)], dim=1)

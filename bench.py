@@ -268,8 +268,8 @@ def run_ours(args):
     # ---------------- measured MAC-pipe peaks (roofline denominators) ----------------
     peaks = {}
     names = dict(MAC_NAMES)
-    names[7] = "imma_s8_mma_sync"
-    for kind in (MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64, 7):
+    names[16] = "imma_s8_mma_sync"
+    for kind in (MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64, 16):
         D.microbench(kind, 148 * 4, 256, 64)  # warm
         best = 0.0
         for _ in range(3):

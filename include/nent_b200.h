@@ -44,6 +44,12 @@ extern "C" {
 #define NENT_MAC_S64 4 /* split x = hi*2^32+lo: IMAD.WIDE + IMAD, |g| < 2^31            */
 #define NENT_MAC_G64 5 /* generic 64x64 low product (mul.lo.u64)                        */
 #define NENT_MAC_X128 6 /* exact 128-bit accumulation + overflow count (object path)    */
+/* Tensor-core digit slicing: x and g split into balanced base-256 int8 digits
+ * (np planes of x, ng digits of g), every digit pair convolved with
+ * mma.sync m16n8k32 s8 (int32 exact), recombined mod 2^64.  Exact whenever the
+ * result fits int64, np <= 8, ng <= 4, K + 15 < 65536. */
+#define NENT_MAC_IMMA 7
+#define NENT_MAC_IMMA_DIGITS(np, ng) (NENT_MAC_IMMA | ((np) << 8) | ((ng) << 12))
 
 /* Elementwise op codes (ops.py:193-204). */
 #define NENT_EW_ADD 0
@@ -194,7 +200,7 @@ int nent_checksum_recover(const void *const *x, int x_bits, const void *cs, int 
 
 /* ---- measurement ------------------------------------------------------------ */
 
-#define NENT_BENCH_IMMA 7 /* microbenchmark only: mma.sync m16n8k32 s8 (legacy IMMA) */
+#define NENT_BENCH_IMMA 16 /* microbenchmark only: mma.sync m16n8k32 s8 (legacy IMMA) */
 
 /* Integer / FP64 pipe microbenchmark used for the roofline denominators.
  * kind: NENT_MAC_* flavour or NENT_BENCH_IMMA; launches blocks x threads threads each doing

@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import MAC_F64, MAC_G64, MAC_I32, MAC_S64, MAC_W64, MAC_X128, bits, call, ptr, row_ptrs
+from ._lib import (MAC_F64, MAC_G64, MAC_I32, MAC_S64, MAC_W64, MAC_X128, bits, call, imma_flavor,
+                   is_imma, ptr, row_ptrs)
 from .errors import DeviceError, ParameterError
 
 _I64_MIN = -(1 << 63)
@@ -68,11 +69,25 @@ def host_max_abs(a: np.ndarray) -> int:
     return max(abs(lo), abs(hi))
 
 
-def pick_flavor(max_x: int, sum_g: int, max_g: int) -> int:
-    """Narrowest MAC flavour that is exact for |x| <= max_x and the given taps.
+def signed_digits(maxabs: int) -> int:
+    """Balanced base-256 int8 digits needed for every |v| <= maxabs."""
+    p = 1
+    while 127 * (256 ** p - 1) // 255 < maxabs:
+        p += 1
+    return p
 
-    bound = max_x * max(sum_g, 1) bounds every partial sum (ops.py:163).
-    """
+
+# measured on B200 (bench.py microbenchmarks, MAC/s): the pipe peaks that
+# decide which exact flavour is fastest for given operand widths
+PIPE_PEAK = {MAC_I32: 16.9e12, MAC_F64: 13.0e12, MAC_W64: 8.2e12, MAC_S64: 5.35e12,
+             MAC_G64: 3.4e12, "imma": 559e12}
+IMMA_EFFICIENCY = 0.5  # fraction of the mma.sync peak the digit-sliced kernel reaches
+
+
+def cuda_core_flavor(max_x: int, sum_g: int, max_g: int) -> int:
+    """Narrowest CUDA-core MAC flavour exact for |x| <= max_x and the taps.
+
+    bound = max_x * max(sum_g, 1) bounds every partial sum (ops.py:163)."""
     bound = max_x * max(sum_g, 1)
     if bound >= 1 << 62:
         return MAC_X128
@@ -85,6 +100,22 @@ def pick_flavor(max_x: int, sum_g: int, max_g: int) -> int:
     if max_g < 1 << 31:
         return MAC_S64
     return MAC_G64
+
+
+def pick_flavor(max_x: int, sum_g: int, max_g: int, K: int | None = None,
+                allow_imma: bool = True) -> int:
+    """Fastest exact flavour.  Every candidate is exact for these bounds; the
+    IMMA digit-sliced tensor-core conv is chosen when its modelled rate
+    (mma.sync peak x efficiency x K/KD / (np*ng)) beats the CUDA-core pipe."""
+    core = cuda_core_flavor(max_x, sum_g, max_g)
+    if not allow_imma or K is None or core == MAC_X128 or K + 15 >= 1 << 16:
+        return core
+    np_, ng = signed_digits(max_x), signed_digits(max_g)
+    if np_ > 8 or ng > 4:
+        return core
+    KD = (K + 15 + 31) // 32 * 32
+    imma_rate = PIPE_PEAK["imma"] * IMMA_EFFICIENCY * K / KD / (np_ * ng)
+    return imma_flavor(np_, ng) if imma_rate > PIPE_PEAK[core] else core
 
 
 def taps_tensor(g, flavor: int | None = None) -> torch.Tensor:

@@ -17,9 +17,29 @@ from .errors import DeviceError, ParameterError, RangeError
 LIB_PATH = Path(__file__).resolve().parent / "libnent_b200.so"
 
 NENT_OK, NENT_ERR_PARAM, NENT_ERR_RANGE, NENT_ERR_CUDA, NENT_ERR_OVERFLOW = 0, 1, 2, 3, 4
-MAC_I32, MAC_F64, MAC_W64, MAC_S64, MAC_G64, MAC_X128 = 1, 2, 3, 4, 5, 6
-MAC_NAMES = {MAC_I32: "i32", MAC_F64: "f64", MAC_W64: "w64", MAC_S64: "s64", MAC_G64: "g64",
-             MAC_X128: "x128"}
+MAC_I32, MAC_F64, MAC_W64, MAC_S64, MAC_G64, MAC_X128, MAC_IMMA = 1, 2, 3, 4, 5, 6, 7
+BENCH_IMMA = 16
+
+
+def imma_flavor(np_: int, ng: int) -> int:
+    """NENT_MAC_IMMA_DIGITS(np, ng): tensor-core digit slicing with np planes of x
+    and ng digits of g (balanced base-256)."""
+    return MAC_IMMA | (np_ << 8) | (ng << 12)
+
+
+def is_imma(flavor: int) -> bool:
+    return (flavor & 0xFF) == MAC_IMMA
+
+
+class _FlavorNames(dict):
+    def __missing__(self, key):
+        if is_imma(key):
+            return f"imma{(key >> 8) & 15}x{(key >> 12) & 15}"
+        raise KeyError(key)
+
+
+MAC_NAMES = _FlavorNames({MAC_I32: "i32", MAC_F64: "f64", MAC_W64: "w64", MAC_S64: "s64",
+                          MAC_G64: "g64", MAC_X128: "x128", BENCH_IMMA: "imma_s8_mma_sync"})
 EW_ADD, EW_SUB, EW_MUL = 0, 1, 2
 
 _P = ctypes.c_void_p

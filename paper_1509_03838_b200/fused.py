@@ -46,9 +46,11 @@ def _eps_bound(max_c: int, p: CodecParams) -> int:
     return max_c * ((1 << p.l) + 1)
 
 
-def conv_flavor(max_x: int, g: np.ndarray) -> int:
+def conv_flavor(max_x: int, g: np.ndarray, allow_imma: bool = True) -> int:
+    """Fastest exact MAC flavour for |x| <= max_x convolved with taps g."""
     g = np.asarray(g, dtype=np.int64)
-    return D.pick_flavor(max_x, int(np.abs(g.astype(object)).sum()), D.host_max_abs(g))
+    return D.pick_flavor(max_x, int(np.abs(g.astype(object)).sum()), D.host_max_abs(g),
+                         K=len(g), allow_imma=allow_imma)
 
 
 def _prep(block: StreamBlock, dtype=None) -> tuple[torch.Tensor, bool]:

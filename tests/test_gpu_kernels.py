@@ -10,7 +10,8 @@ import torch
 import paper_1509_03838_b200 as nent
 from paper_1509_03838_b200 import _device as D
 from paper_1509_03838_b200 import fused
-from paper_1509_03838_b200._lib import MAC_F64, MAC_G64, MAC_I32, MAC_S64, MAC_W64, MAC_X128
+from paper_1509_03838_b200._lib import (MAC_F64, MAC_G64, MAC_I32, MAC_S64, MAC_W64, MAC_X128,
+                                        imma_flavor, is_imma)
 
 pytestmark = pytest.mark.gpu
 
@@ -34,7 +35,37 @@ def exact_flavors(max_x, g):
         out.append(MAC_W64)
     if mg < 1 << 31:
         out.append(MAC_S64)
+    np_, ng = D.signed_digits(max_x), D.signed_digits(mg)
+    if ng <= 4 and np_ <= 8 and len(g) + 15 < 1 << 16 and b < 1 << 62:
+        out.append(imma_flavor(np_, ng))
     return out
+
+
+@pytest.mark.parametrize("bits_x,bits_g", [(7, 7), (8, 8), (12, 12), (20, 9), (33, 12), (40, 20),
+                                           (50, 30), (61, 1)])
+def test_imma_digit_widths(oracle, bits_x, bits_g):
+    """Digit slicing is exact for every operand width up to the int64 result."""
+    K = 77
+    x = rand(bits_x * 100 + bits_g, (3, 3000), -(1 << bits_x) + 1, (1 << bits_x) - 1)
+    g = rand(bits_g, (K,), -(1 << bits_g) + 1, (1 << bits_g) - 1)
+    bound = (1 << bits_x) * int(np.abs(g).sum())
+    if bound >= 1 << 62:
+        pytest.skip("result may exceed int64")
+    ref = oracle.full_conv(x, g)
+    fl = imma_flavor(D.signed_digits(int(np.abs(x).max())), D.signed_digits(int(np.abs(g).max())))
+    y, _ = D.conv(torch.from_numpy(x).cuda(), D.taps_tensor(g, fl), K, fl, period=3000 + K - 1)
+    assert np.array_equal(y.cpu().numpy(), ref), (bits_x, bits_g)
+
+
+def test_imma_max_digits_and_extremes(oracle):
+    # every digit saturated: values at +-(2^(8np-1) - ...) and taps at the int8 edges
+    x = np.full((2, 700), 127 * (256 ** 3 - 1) // 255, dtype=np.int64)
+    x[1, ::2] = -128 * (256 ** 3 - 1) // 255
+    g = np.array([127, -128, 127, -128, 1], dtype=np.int64)
+    ref = oracle.circ_conv(x, g)
+    fl = imma_flavor(3, 1)
+    y, _ = D.conv(torch.from_numpy(x).cuda(), D.taps_tensor(g, fl), 5, fl)
+    assert np.array_equal(y.cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("n,K", [(1, 1), (5, 1), (7, 7), (100, 33), (1537, 64), (5000, 256),
@@ -112,7 +143,8 @@ def test_fused_conv_every_failure(oracle, m, w):
     ref = oracle.full_conv(c, g)
     block = nent.StreamBlock(p, c)
     eb = bound * ((1 << p.l) + 1)
-    for flavor in [f for f in exact_flavors(eb, g) if f in (MAC_I32, MAC_F64, MAC_W64, MAC_S64)]:
+    for flavor in [f for f in exact_flavors(eb, g)
+                   if f in (MAC_I32, MAC_F64, MAC_W64, MAC_S64) or is_imma(f)]:
         for r in [None] + list(range(m)):
             res = fused.entangled_conv(block, g, failed=r, flavor=flavor)
             assert np.array_equal(res.outputs.data, ref), (m, w, flavor, r)

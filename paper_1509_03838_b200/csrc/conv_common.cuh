@@ -1,0 +1,100 @@
+// conv_common.cuh -- argument block and on-load input chain shared by the
+// CUDA-core (conv.cu) and tensor-core (conv_imma.cu) convolution kernels.
+#pragma once
+#include "common.cuh"
+
+namespace nent {
+
+struct ConvArgs {
+  Rows a;        // optional shifted operand rows: x = (a << l) + b
+  Rows b;        // main operand rows
+  MutRows y;     // output rows (delta rows, or the m recovered rows when fused)
+  int rows;      // streams (== m when fused)
+  int in_bits, y_bits, g_bits, add_bits;
+  int l;
+  int K, Kp, kseg, sstride, gbytes;
+  int r, wide;
+  int64_t n_in, period, y_begin, n_out;
+  int64_t scale;
+  const void* add;
+  const int64_t* perm;
+  const void* g;
+  unsigned long long* mismatch;
+};
+
+// x_row[p] after the on-load chain: entangle, scale, add, gather, zero-pad.
+__device__ __forceinline__ int64_t conv_prologue(const ConvArgs& A, int row, int64_t p) {
+  int64_t q = p;
+  if (q < 0 || q >= A.period) {
+    q %= A.period;
+    if (q < 0) q += A.period;
+  }
+  if (q >= A.n_in) return 0;
+  if (A.perm) q = __ldg(A.perm + q);
+  int64_t e = ld_bits(A.b.p[row], A.in_bits, q);
+  const void* ap = A.a.p[row];
+  if (ap) e = wadd(wshl(ld_bits(ap, A.in_bits, q), A.l), e);
+  if (A.scale != 1) e = wmul(e, A.scale);
+  if (A.add) e = wadd(e, ld_bits(A.add, A.add_bits, q));
+  return e;
+}
+
+// Stage NS consecutive input positions p0 .. p0+NS-1 of one row through the
+// on-load chain, calling emit(i, value).  Interior tiles (no wrap, no zero
+// padding) take a batched path: every thread first issues U independent
+// coalesced loads (perm index, a, b, add) and only then computes, so ~U*warps
+// loads are in flight per SM instead of one per warp.  Edge tiles use the
+// general per-element path.
+template <typename TI, int U, typename F>
+__device__ __forceinline__ void stage_interior(const ConvArgs& A, int row, int64_t p0, int NS,
+                                               F&& emit) {
+  const TI* __restrict__ bp = reinterpret_cast<const TI*>(A.b.p[row]);
+  const TI* __restrict__ ap = reinterpret_cast<const TI*>(A.a.p[row]);
+  const int nt = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < NS; i0 += nt * U) {
+    int64_t q[U], vb[U], va[U], vd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nt;
+      q[u] = p0 + (i < NS ? i : 0);
+      if (A.perm) q[u] = __ldg(A.perm + q[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vb[u] = (int64_t)__ldg(bp + q[u]);
+      va[u] = ap ? (int64_t)__ldg(ap + q[u]) : 0;
+      vd[u] = A.add ? ld_bits(A.add, A.add_bits, q[u]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nt;
+      if (i < NS) {
+        int64_t e = vb[u];
+        if (ap) e = wadd(wshl(va[u], A.l), e);
+        if (A.scale != 1) e = wmul(e, A.scale);
+        if (A.add) e = wadd(e, vd[u]);
+        emit(i, e);
+      }
+    }
+  }
+}
+
+template <int U, typename F>
+__device__ __forceinline__ void stage_row(const ConvArgs& A, int row, int64_t p0, int NS, F&& emit) {
+  if (row >= A.rows) {
+    for (int i = threadIdx.x; i < NS; i += blockDim.x) emit(i, 0);
+    return;
+  }
+  if (p0 >= 0 && p0 + NS <= A.n_in) {
+    if (A.in_bits == 32) stage_interior<int32_t, U>(A, row, p0, NS, emit);
+    else stage_interior<int64_t, U>(A, row, p0, NS, emit);
+    return;
+  }
+  for (int i = threadIdx.x; i < NS; i += blockDim.x) emit(i, conv_prologue(A, row, p0 + i));
+}
+
+
+// tensor-core digit-sliced convolution (conv_imma.cu)
+int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s);
+
+}  // namespace nent

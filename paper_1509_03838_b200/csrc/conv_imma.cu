@@ -1,0 +1,300 @@
+// conv_imma.cu -- exact integer convolution on the tensor cores by digit
+// slicing (mma.sync m16n8k32 s8 -> s32), plain or fused with entangle/extract.
+// Reference semantics: ops._circ_conv_rows (/root/reference/pkg/src/nent/ops.py:158-172).
+#include "common.cuh"
+#include "conv_common.cuh"
+#include "recover.cuh"
+
+namespace nent {
+
+// ============================================================================
+// IMMA digit-sliced exact convolution (tensor cores, mma.sync s8*s8+s32).
+//
+// Every operand is split into balanced base-256 digits (int8 in [-128,127]):
+//   x = sum_p 256^p x_p  (NP planes),   g = sum_j 256^j g_j  (NG digits)
+//   y = sum_{p,j} 256^(p+j) (x_p (*) g_j)          (mod 2^64: exact whenever
+//                                                   y fits int64)
+// Each digit convolution is an int8 GEMM with int32 accumulation (exact:
+// |partial| <= 2^14 * KD < 2^31 for KD < 2^17).  The GEMM is Toeplitz:
+//   Y[a, b] = sum_t A[a, t] B[t, b],  output j0 + 16a + b (b in [0,16))
+//   A[a, t] = x_p[j0 + 16a + t - (K-1)]   (Hankel: row a is the signal shifted
+//                                          by 16 bytes, i.e. one smem row)
+//   B[t, b] = g_j[b + K - 1 - t]          (the taps, built once per CTA)
+// Because consecutive Hankel rows are exactly 16 bytes apart, ldmatrix reads
+// A fragments straight from the digit plane in shared memory (8 rows x 16 B
+// = 128 contiguous bytes per 8x8 matrix: conflict-free) -- the Hankel matrix
+// is never materialised.  B fragments stay in registers for a K-segment.
+// Warp w owns RT row-tiles of 16 rows (256 outputs each); per (plane, kc) it
+// issues one ldmatrix.x4 and 2*NG MMAs per row-tile.  After each plane the
+// int32 accumulators are folded into int64 (shift by 8(p+j)); the per-stream
+// int64 results meet in shared memory, where the epilogue stores them or runs
+// the m-stream recovery (fused entangle -> conv -> extract).
+// ============================================================================
+
+constexpr int IM_WARPS = 4;
+constexpr int IM_NT = IM_WARPS * 32;
+
+__host__ __device__ constexpr int imma_rt(int ms) { return ms <= 4 ? 2 : 1; }
+__host__ __device__ constexpr int imma_seg(int ng) { return ng == 1 ? 18 : ng == 2 ? 9 : ng == 3 ? 6 : 4; }
+
+struct ImmaGeom {
+  int KD;    // K-dimension of the Toeplitz GEMM (multiple of 32)
+  int NKC;   // KD / 32
+  int KDs;   // Bt row stride in bytes (== 16 mod 128: conflict-free ldmatrix)
+  int S;     // bytes per digit plane (multiple of 16)
+  int np;    // digit planes of x
+  int bt_off, pl_off, dt_off;  // smem offsets
+  size_t smem;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void imma16832(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// balanced base-256 digit p of v (v = sum_p 256^p digit_p, digits in [-128,127])
+__device__ __forceinline__ uint32_t digit_byte(int64_t& rest) {
+  const int64_t d = (int64_t)(int8_t)(uint8_t)(uint64_t)rest;
+  rest = (int64_t)((uint64_t)rest - (uint64_t)d) >> 8;
+  return (uint32_t)(uint8_t)d;
+}
+
+template <int MS, int NG, bool EXTRACT>
+__global__ void __launch_bounds__(IM_NT, 1)
+    conv_imma_kernel(const __grid_constant__ ConvArgs A, const ImmaGeom Gm) {
+  constexpr int RT = imma_rt(MS);
+  constexpr int SEG = imma_seg(NG);
+  constexpr int T = IM_WARPS * RT * 256;  // outputs per CTA tile
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* bt = smem + Gm.bt_off;   // NG x 16 rows x KDs
+  unsigned char* pl = smem + Gm.pl_off;   // MS x np planes x S bytes
+  int64_t* dt = reinterpret_cast<int64_t*>(smem + Gm.dt_off);  // MS x T
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j0 = A.y_begin + (int64_t)blockIdx.x * T;
+  const int row0 = EXTRACT ? 0 : (int)blockIdx.y * MS;
+  const int np = Gm.np, KDs = Gm.KDs, S = Gm.S;
+
+  // ---- digit planes: smem byte i <-> input position j0 - (K-1) + i ----
+  const int64_t p0 = j0 - (A.K - 1);
+  for (int s = 0; s < MS; ++s) {
+    unsigned char* ps = pl + (size_t)s * np * S;
+    stage_row<8>(A, row0 + s, p0, S, [&](int i, int64_t v) {
+      int64_t rest = v;
+      for (int p = 0; p < np; ++p) ps[(size_t)p * S + i] = (unsigned char)digit_byte(rest);
+    });
+  }
+
+  const uint32_t pl_s = (uint32_t)__cvta_generic_to_shared(pl);
+  const uint32_t bt_s = (uint32_t)__cvta_generic_to_shared(bt);
+  const int mat = lane >> 3, r8 = lane & 7;
+  // per-lane ldmatrix row offsets
+  const uint32_t a_lane = 16u * (uint32_t)(r8 + 8 * (mat & 1)) + 16u * (uint32_t)(mat >> 1);
+  const uint32_t b_lane = (uint32_t)((8 * (mat >> 1) + r8) * KDs + 16 * (mat & 1));
+  const int g = lane >> 2, t4 = lane & 3;
+
+  // K is consumed SEG*32 Toeplitz columns at a time: the segment's taps are
+  // digit-split into Bt (shared), its B fragments held in registers, and
+  // every stream's int64 partial results accumulate in the staging tile dt.
+  for (int kc0 = 0; kc0 < Gm.NKC; kc0 += SEG) {
+    const int nkc = min(SEG, Gm.NKC - kc0);
+    __syncthreads();  // previous segment's readers of Bt are done
+    // Bt_j[b][tl] = digit_j(g[b + K - 1 - t]), t = 32*kc0 + tl
+    for (int i = tid; i < 16 * 32 * nkc; i += IM_NT) {
+      const int b = i / (32 * nkc), tl = i - b * 32 * nkc;
+      const int k = b + A.K - 1 - (32 * kc0 + tl);
+      int64_t rest = (k >= 0 && k < A.K) ? ld_bits(A.g, A.g_bits, k) : 0;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) bt[(j * 16 + b) * KDs + tl] = (unsigned char)digit_byte(rest);
+    }
+    __syncthreads();
+    uint32_t bf[SEG][NG][4];  // per kc: {b0,b1} of n8-tile 0, {b0,b1} of n8-tile 1
+#pragma unroll
+    for (int kk = 0; kk < SEG; ++kk)
+#pragma unroll
+      for (int j = 0; j < NG; ++j)
+        if (kk < nkc) ldsm_x4(bf[kk][j], bt_s + (uint32_t)(j * 16 * KDs) + b_lane + 32u * (uint32_t)kk);
+
+    for (int s = 0; s < MS; ++s) {
+      if (!EXTRACT && row0 + s >= A.rows) break;
+      long long acc[RT][2][4];
+#pragma unroll
+      for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[rt][nb][q] = 0;
+      for (int p = 0; p < np; ++p) {
+        const uint32_t plane = pl_s + (uint32_t)((s * np + p) * S) + 32u * (uint32_t)kc0;
+        int c[RT][2][NG][4];
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) c[rt][nb][j][q] = 0;
+#pragma unroll
+        for (int kk = 0; kk < SEG; ++kk) {
+          if (kk >= nkc) break;
+#pragma unroll
+          for (int rt = 0; rt < RT; ++rt) {
+            uint32_t af[4];
+            ldsm_x4(af, plane + 256u * (uint32_t)(warp * RT + rt) + a_lane + 32u * (uint32_t)kk);
+#pragma unroll
+            for (int j = 0; j < NG; ++j) {
+              imma16832(c[rt][0][j], af, bf[kk][j][0], bf[kk][j][1]);
+              imma16832(c[rt][1][j], af, bf[kk][j][2], bf[kk][j][3]);
+            }
+          }
+        }
+        // fold the int32 digit products into the int64 accumulators
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint64_t v = 0;
+#pragma unroll
+              for (int j = 0; j < NG; ++j) v += (uint64_t)(int64_t)c[rt][nb][j][q] << (8 * j);
+              acc[rt][nb][q] = (long long)((uint64_t)acc[rt][nb][q] + (v << (8 * p)));
+            }
+      }
+      // this segment's contribution: C fragment (row g|g+8, col 2t|2t+1) of n8-tile nb
+#pragma unroll
+      for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int u = 256 * (warp * RT + rt) + 16 * (g + 8 * (q >> 1)) + 8 * nb + 2 * t4 + (q & 1);
+            int64_t* d = dt + (size_t)s * T + u;
+            *d = kc0 == 0 ? acc[rt][nb][q] : wadd(*d, acc[rt][nb][q]);
+          }
+    }
+  }
+  __syncthreads();
+
+  // ---- epilogue: coalesced stores or the fused m-stream recovery ----
+  const int64_t jend = A.y_begin + A.n_out;
+  if (!EXTRACT) {
+    for (int s = 0; s < MS; ++s) {
+      const int row = row0 + s;
+      if (row >= A.rows) break;
+      for (int u = tid; u < T; u += IM_NT) {
+        const int64_t j = j0 + u;
+        if (j < jend) st_bits(A.y.p[row], A.y_bits, j - A.y_begin, dt[(size_t)s * T + u]);
+      }
+    }
+  } else {
+    const bool verify = A.r < 0;
+    const int pivot = verify ? 0 : A.r;
+    unsigned bad = 0;
+    for (int u = tid; u < T; u += IM_NT) {
+      const int64_t j = j0 + u;
+      if (j >= jend) break;
+      int64_t dl[MS], orot[MS];
+#pragma unroll
+      for (int s = 0; s < MS; ++s) dl[s] = dt[(size_t)s * T + u];
+      recover_regs_valid<MS>(dl, pivot, A.l, orot);
+      if (verify) bad += (dl[0] != wadd(wshl(orot[MS - 1], A.l), orot[0])) ? 1u : 0u;
+#pragma unroll
+      for (int t = 0; t < MS; ++t) {
+        int row = pivot + t;
+        row -= row >= MS ? MS : 0;
+        st_bits(A.y.p[row], A.y_bits, j - A.y_begin, orot[t]);
+      }
+    }
+    if (A.mismatch) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      if (lane == 0 && bad) atomicAdd(A.mismatch, (unsigned long long)bad);
+    }
+  }
+}
+
+template <int MS, int NG, bool EXTRACT>
+static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
+  constexpr int T = IM_WARPS * imma_rt(MS) * 256;
+  ImmaGeom Gm{};
+  Gm.np = np;
+  Gm.KD = (A.K + 15 + 31) / 32 * 32;
+  Gm.NKC = Gm.KD / 32;
+  Gm.KDs = (imma_seg(NG) * 32 + 127) / 128 * 128 + 16;  // one segment; == 16 mod 128
+  Gm.S = (T + Gm.KD + 15) / 16 * 16;
+  Gm.bt_off = 0;
+  Gm.pl_off = (NG * 16 * Gm.KDs + 127) / 128 * 128;
+  Gm.dt_off = (Gm.pl_off + MS * np * Gm.S + 127) / 128 * 128;
+  Gm.smem = (size_t)Gm.dt_off + (size_t)MS * T * 8;
+  if (Gm.smem > 227 * 1024) {
+    set_error("imma conv: tile needs %zu bytes of shared memory (K=%d too long)", Gm.smem, A.K);
+    return NENT_ERR_PARAM;
+  }
+  auto kern = conv_imma_kernel<MS, NG, EXTRACT>;
+  static size_t configured = 0;
+  if (Gm.smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm.smem) !=
+        cudaSuccess) {
+      set_error("imma conv: cannot reserve %zu bytes of shared memory", Gm.smem);
+      return NENT_ERR_CUDA;
+    }
+    configured = Gm.smem;
+  }
+  const int64_t tiles = (A.n_out + T - 1) / T;
+  dim3 grid((unsigned)tiles, EXTRACT ? 1 : (unsigned)((A.rows + MS - 1) / MS));
+  kern<<<grid, IM_NT, Gm.smem, stream>>>(A, Gm);
+  return check_launch("imma conv");
+}
+
+template <int NG>
+static int imma_dispatch_ng(ConvArgs& A, int np, bool extract, cudaStream_t s) {
+  if (extract) {
+    switch (A.rows) {
+      case 3: return launch_imma<3, NG, true>(A, np, s);
+      case 4: return launch_imma<4, NG, true>(A, np, s);
+      case 5: return launch_imma<5, NG, true>(A, np, s);
+      case 6: return launch_imma<6, NG, true>(A, np, s);
+      case 7: return launch_imma<7, NG, true>(A, np, s);
+      case 8: return launch_imma<8, NG, true>(A, np, s);
+    }
+    set_error("imma fused conv: m=%d not in 3..8", A.rows);
+    return NENT_ERR_PARAM;
+  }
+  switch (A.rows) {
+    case 1: return launch_imma<1, NG, false>(A, np, s);
+    case 2: return launch_imma<2, NG, false>(A, np, s);
+    case 3: return launch_imma<3, NG, false>(A, np, s);
+    default: return launch_imma<4, NG, false>(A, np, s);
+  }
+}
+
+// flavor word: NENT_MAC_IMMA | np << 8 | ng << 12
+int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
+  const int np = (flavor >> 8) & 0xf, ng = (flavor >> 12) & 0xf;
+  if (np < 1 || np > 8 || ng < 1 || ng > 4) {
+    set_error("imma conv: digit counts np=%d ng=%d outside 1..8 / 1..4", np, ng);
+    return NENT_ERR_PARAM;
+  }
+  if (A.K + 15 > (1 << 16)) {
+    set_error("imma conv: K=%d too long for int32 digit sums", A.K);
+    return NENT_ERR_PARAM;
+  }
+  switch (ng) {
+    case 1: return imma_dispatch_ng<1>(A, np, extract, s);
+    case 2: return imma_dispatch_ng<2>(A, np, extract, s);
+    case 3: return imma_dispatch_ng<3>(A, np, extract, s);
+    default: return imma_dispatch_ng<4>(A, np, extract, s);
+  }
+}
+
+}  // namespace nent

@@ -33,7 +33,8 @@ def bench(fn, reps=20):
     return a.elapsed_time(b) / reps
 
 
-for cfg in (1, 2, 3, 5):
+CFGS = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 5]
+for cfg in CFGS:
     wl = workloads.make(cfg)
     p = wl.params
     c = torch.from_numpy(wl.c).cuda().to(torch.int32)

@@ -38,6 +38,7 @@ __host__ __device__ constexpr int imma_rt(int ms) { return ms <= 4 ? 2 : 1; }
 __host__ __device__ constexpr int imma_seg(int ng) { return ng == 1 ? 18 : ng == 2 ? 9 : ng == 3 ? 6 : 4; }
 
 struct ImmaGeom {
+  int Keff;  // K + zero taps so that every tile's first staged position is 4-aligned
   int KD;    // K-dimension of the Toeplitz GEMM (multiple of 32)
   int NKC;   // KD / 32
   int KDs;   // Bt row stride in bytes (== 16 mod 128: conflict-free ldmatrix)
@@ -61,11 +62,20 @@ __device__ __forceinline__ void imma16832(int (&c)[4], const uint32_t (&a)[4], u
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// balanced base-256 digit p of v (v = sum_p 256^p digit_p, digits in [-128,127])
-__device__ __forceinline__ uint32_t digit_byte(int64_t& rest) {
-  const int64_t d = (int64_t)(int8_t)(uint8_t)(uint64_t)rest;
-  rest = (int64_t)((uint64_t)rest - (uint64_t)d) >> 8;
-  return (uint32_t)(uint8_t)d;
+// Balanced base-256 digits without a carry chain: with u = v + sum_p 128*256^p
+// (mod 2^64), u's bytes are d_p + 128 in [0, 255], so the int8 digit d_p is
+// byte p of (u XOR 0x8080...80).  One 64-bit add + xor yields all 8 digits.
+__device__ __forceinline__ uint64_t digit_word(int64_t v, uint64_t bias) {
+  return ((uint64_t)v + bias) ^ 0x8080808080808080ull;
+}
+__host__ __device__ constexpr uint64_t digit_bias(int np) {
+  return np >= 8 ? 0x8080808080808080ull : (0x8080808080808080ull & ((1ull << (8 * np)) - 1));
+}
+// byte p of each of 4 words, packed little-endian into one word
+__device__ __forceinline__ uint32_t gather_byte(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                                int p) {
+  const uint32_t sel = (uint32_t)p | ((uint32_t)(p + 4) << 4);
+  return __byte_perm(__byte_perm(w0, w1, sel), __byte_perm(w2, w3, sel), 0x5410);
 }
 
 template <int MS, int NG, bool EXTRACT>
@@ -83,14 +93,49 @@ __global__ void __launch_bounds__(IM_NT, 1)
   const int row0 = EXTRACT ? 0 : (int)blockIdx.y * MS;
   const int np = Gm.np, KDs = Gm.KDs, S = Gm.S;
 
-  // ---- digit planes: smem byte i <-> input position j0 - (K-1) + i ----
-  const int64_t p0 = j0 - (A.K - 1);
+  // ---- digit planes: smem byte i <-> input position j0 - (Keff-1) + i ----
+  // Keff = K + zero taps chosen so p0 is a multiple of 4 for every tile:
+  // interior tiles then stage with 16-byte vector loads.
+  const int64_t p0 = j0 - (Gm.Keff - 1);
+  const uint64_t xbias = digit_bias(np);
   for (int s = 0; s < MS; ++s) {
-    unsigned char* ps = pl + (size_t)s * np * S;
-    stage_row<8>(A, row0 + s, p0, S, [&](int i, int64_t v) {
-      int64_t rest = v;
-      for (int p = 0; p < np; ++p) ps[(size_t)p * S + i] = (unsigned char)digit_byte(rest);
-    });
+    const int row = row0 + s;
+    uint32_t* ps = reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S);
+    const int S4 = S >> 2, P4 = np * S4;  // words per plane / per stream
+    const bool live = row < A.rows;
+    const bool vec = live && A.in_bits == 32 && !A.perm && A.scale == 1 && !A.add && p0 >= 0 &&
+                     p0 + S <= A.n_in && ((uintptr_t)A.b.p[row] & 15) == 0 &&
+                     (!A.a.p[row] || ((uintptr_t)A.a.p[row] & 15) == 0);
+    for (int w = tid; w < S4; w += IM_NT) {
+      int64_t v[4];
+      if (vec) {
+        const int4 bv = __ldg(reinterpret_cast<const int4*>(A.b.p[row]) + (p0 >> 2) + w);
+        v[0] = bv.x; v[1] = bv.y; v[2] = bv.z; v[3] = bv.w;
+        if (A.a.p[row]) {
+          const int4 av = __ldg(reinterpret_cast<const int4*>(A.a.p[row]) + (p0 >> 2) + w);
+          v[0] = wadd(wshl(av.x, A.l), v[0]); v[1] = wadd(wshl(av.y, A.l), v[1]);
+          v[2] = wadd(wshl(av.z, A.l), v[2]); v[3] = wadd(wshl(av.w, A.l), v[3]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = live ? conv_prologue(A, row, p0 + 4 * w + e) : 0;
+      }
+      uint64_t u[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) u[e] = digit_word(v[e], xbias);
+      const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
+      if (np > 4) {
+        const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32),
+                       h2 = (uint32_t)(u[2] >> 32), h3 = (uint32_t)(u[3] >> 32);
+#pragma unroll
+        for (int p = 4; p < 8; ++p)
+          if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
+      }
+    }
+    (void)P4;
   }
 
   const uint32_t pl_s = (uint32_t)__cvta_generic_to_shared(pl);
@@ -107,13 +152,18 @@ __global__ void __launch_bounds__(IM_NT, 1)
   for (int kc0 = 0; kc0 < Gm.NKC; kc0 += SEG) {
     const int nkc = min(SEG, Gm.NKC - kc0);
     __syncthreads();  // previous segment's readers of Bt are done
-    // Bt_j[b][tl] = digit_j(g[b + K - 1 - t]), t = 32*kc0 + tl
-    for (int i = tid; i < 16 * 32 * nkc; i += IM_NT) {
-      const int b = i / (32 * nkc), tl = i - b * 32 * nkc;
-      const int k = b + A.K - 1 - (32 * kc0 + tl);
-      int64_t rest = (k >= 0 && k < A.K) ? ld_bits(A.g, A.g_bits, k) : 0;
+    // Bt_j[b][tl] = digit_j(g[b + Keff - 1 - t]), t = 32*kc0 + tl
+    {
+      const int W = 32 * nkc;
+      const int kbase = Gm.Keff - 1 - 32 * kc0;
+      for (int b = 0; b < 16; ++b)
+        for (int tl = tid; tl < W; tl += IM_NT) {
+          const int k = b + kbase - tl;
+          const int64_t gv = (k >= 0 && k < A.K) ? ld_bits(A.g, A.g_bits, k) : 0;
+          const uint64_t u = digit_word(gv, digit_bias(NG));
 #pragma unroll
-      for (int j = 0; j < NG; ++j) bt[(j * 16 + b) * KDs + tl] = (unsigned char)digit_byte(rest);
+          for (int j = 0; j < NG; ++j) bt[(j * 16 + b) * KDs + tl] = (unsigned char)(u >> (8 * j));
+        }
     }
     __syncthreads();
     uint32_t bf[SEG][NG][4];  // per kc: {b0,b1} of n8-tile 0, {b0,b1} of n8-tile 1
@@ -143,9 +193,7 @@ __global__ void __launch_bounds__(IM_NT, 1)
             for (int j = 0; j < NG; ++j)
 #pragma unroll
               for (int q = 0; q < 4; ++q) c[rt][nb][j][q] = 0;
-#pragma unroll
-        for (int kk = 0; kk < SEG; ++kk) {
-          if (kk >= nkc) break;
+        auto kstep = [&](int kk) {
 #pragma unroll
           for (int rt = 0; rt < RT; ++rt) {
             uint32_t af[4];
@@ -155,6 +203,18 @@ __global__ void __launch_bounds__(IM_NT, 1)
               imma16832(c[rt][0][j], af, bf[kk][j][0], bf[kk][j][1]);
               imma16832(c[rt][1][j], af, bf[kk][j][2], bf[kk][j][3]);
             }
+          }
+        };
+        if (nkc == SEG) {
+          // full segment: straight-line code, so the A-fragment loads of the
+          // next k-steps can be scheduled ahead of this step's MMAs
+#pragma unroll
+          for (int kk = 0; kk < SEG; ++kk) kstep(kk);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < SEG; ++kk) {
+            if (kk >= nkc) break;
+            kstep(kk);
           }
         }
         // fold the int32 digit products into the int64 accumulators
@@ -228,7 +288,9 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
   constexpr int T = IM_WARPS * imma_rt(MS) * 256;
   ImmaGeom Gm{};
   Gm.np = np;
-  Gm.KD = (A.K + 15 + 31) / 32 * 32;
+  // p0 = y_begin + tile*T - (Keff - 1) must be == 0 mod 4 (T is a multiple of 16)
+  Gm.Keff = A.K + (int)((((A.y_begin - A.K + 1) % 4) + 4) % 4);
+  Gm.KD = (Gm.Keff + 15 + 31) / 32 * 32;
   Gm.NKC = Gm.KD / 32;
   Gm.KDs = (imma_seg(NG) * 32 + 127) / 128 * 128 + 16;  // one segment; == 16 mod 128
   Gm.S = (T + Gm.KD + 15) / 16 * 16;

@@ -44,7 +44,8 @@ struct ImmaGeom {
   int KDs;   // Bt row stride in bytes (== 16 mod 128: conflict-free ldmatrix)
   int S;     // bytes per digit plane (multiple of 16)
   int np;    // digit planes of x
-  int bt_off, pl_off, dt_off;  // smem offsets
+  int RS;    // bytes per reversed-tap digit row
+  int bt_off, pl_off, dt_off, r_off;  // smem offsets
   size_t smem;
 };
 
@@ -94,48 +95,95 @@ __global__ void __launch_bounds__(IM_NT, 1)
   const int np = Gm.np, KDs = Gm.KDs, S = Gm.S;
 
   // ---- digit planes: smem byte i <-> input position j0 - (Keff-1) + i ----
-  // Keff = K + zero taps chosen so p0 is a multiple of 4 for every tile:
-  // interior tiles then stage with 16-byte vector loads.
+  // Keff = K + zero taps chosen so p0 is a multiple of 4 for every tile.
   const int64_t p0 = j0 - (Gm.Keff - 1);
   const uint64_t xbias = digit_bias(np);
+  const int S4 = S >> 2;
+  // Fast path (interior tile, int32 streams, no gather/scale/add): one TMA
+  // bulk copy per stream lands the raw tile in shared memory (aliasing the
+  // result tile dt, unused until the MMAs finish), then the digit split runs
+  // from shared memory.  Edge tiles take the general per-element chain.
+  bool fast = A.in_bits == 32 && !A.perm && A.scale == 1 && !A.add && p0 >= 0 && p0 + S <= A.n_in;
+#pragma unroll
   for (int s = 0; s < MS; ++s) {
     const int row = row0 + s;
-    uint32_t* ps = reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S);
-    const int S4 = S >> 2, P4 = np * S4;  // words per plane / per stream
-    const bool live = row < A.rows;
-    const bool vec = live && A.in_bits == 32 && !A.perm && A.scale == 1 && !A.add && p0 >= 0 &&
-                     p0 + S <= A.n_in && ((uintptr_t)A.b.p[row] & 15) == 0 &&
-                     (!A.a.p[row] || ((uintptr_t)A.a.p[row] & 15) == 0);
+    fast = fast && row < A.rows && ((uintptr_t)A.b.p[row] & 15) == 0 && (EXTRACT || !A.a.p[row]);
+  }
+  if (fast) {
+    __shared__ __align__(8) uint64_t mbar;
+    int32_t* raw = reinterpret_cast<int32_t*>(smem + Gm.dt_off);  // MS x S words
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)(MS * S * 4);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+#pragma unroll
+      for (int s = 0; s < MS; ++s) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(raw + (size_t)s * S);
+        const int32_t* src = reinterpret_cast<const int32_t*>(A.b.p[row0 + s]) + p0;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst), "l"(src), "r"((uint32_t)(S * 4)), "r"(mb) : "memory");
+      }
+    }
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(mb) : "memory");
+    const int4* raw4 = reinterpret_cast<const int4*>(raw);
     for (int w = tid; w < S4; w += IM_NT) {
-      int64_t v[4];
-      if (vec) {
-        const int4 bv = __ldg(reinterpret_cast<const int4*>(A.b.p[row]) + (p0 >> 2) + w);
-        v[0] = bv.x; v[1] = bv.y; v[2] = bv.z; v[3] = bv.w;
-        if (A.a.p[row]) {
-          const int4 av = __ldg(reinterpret_cast<const int4*>(A.a.p[row]) + (p0 >> 2) + w);
+#pragma unroll
+      for (int s = 0; s < MS; ++s) {
+        const int4 bv = raw4[(size_t)s * S4 + w];
+        int64_t v[4] = {bv.x, bv.y, bv.z, bv.w};
+        if (EXTRACT) {  // eps_s = (c_{s-1} << l) + c_s, both tiles already in smem
+          const int4 av = raw4[(size_t)((s + MS - 1) % MS) * S4 + w];
           v[0] = wadd(wshl(av.x, A.l), v[0]); v[1] = wadd(wshl(av.y, A.l), v[1]);
           v[2] = wadd(wshl(av.z, A.l), v[2]); v[3] = wadd(wshl(av.w, A.l), v[3]);
         }
-      } else {
+        uint32_t* ps = reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S);
+        uint64_t u[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = live ? conv_prologue(A, row, p0 + 4 * w + e) : 0;
-      }
-      uint64_t u[4];
+        for (int e = 0; e < 4; ++e) u[e] = digit_word(v[e], xbias);
+        const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) u[e] = digit_word(v[e], xbias);
-      const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
+        for (int p = 0; p < 4; ++p)
+          if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
+        if (np > 4) {
+          const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32),
+                         h2 = (uint32_t)(u[2] >> 32), h3 = (uint32_t)(u[3] >> 32);
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
-        if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
-      if (np > 4) {
-        const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32),
-                       h2 = (uint32_t)(u[2] >> 32), h3 = (uint32_t)(u[3] >> 32);
-#pragma unroll
-        for (int p = 4; p < 8; ++p)
-          if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
+          for (int p = 4; p < 8; ++p)
+            if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
+        }
       }
     }
-    (void)P4;
+  } else {
+    for (int s = 0; s < MS; ++s) {
+      const int row = row0 + s;
+      uint32_t* ps = reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S);
+      const bool live = row < A.rows;
+      for (int w = tid; w < S4; w += IM_NT) {
+        uint64_t u[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          u[e] = digit_word(live ? conv_prologue(A, row, p0 + 4 * w + e) : 0, xbias);
+        const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+          if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
+        if (np > 4) {
+          const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32),
+                         h2 = (uint32_t)(u[2] >> 32), h3 = (uint32_t)(u[3] >> 32);
+#pragma unroll
+          for (int p = 4; p < 8; ++p)
+            if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
+        }
+      }
+    }
   }
 
   const uint32_t pl_s = (uint32_t)__cvta_generic_to_shared(pl);
@@ -152,18 +200,31 @@ __global__ void __launch_bounds__(IM_NT, 1)
   for (int kc0 = 0; kc0 < Gm.NKC; kc0 += SEG) {
     const int nkc = min(SEG, Gm.NKC - kc0);
     __syncthreads();  // previous segment's readers of Bt are done
-    // Bt_j[b][tl] = digit_j(g[b + Keff - 1 - t]), t = 32*kc0 + tl
+    // Bt_j[b][tl] = digit_j(g[b + Keff - 1 - t]), t = 32*kc0 + tl.  Row b is
+    // the reversed digit sequence R_j[v] = digit_j(g[kbase - v]) shifted by b
+    // bytes: build R_j once (W + 16 bytes), then every Bt word is one funnel
+    // shift of two aligned R_j words.
     {
       const int W = 32 * nkc;
       const int kbase = Gm.Keff - 1 - 32 * kc0;
-      for (int b = 0; b < 16; ++b)
-        for (int tl = tid; tl < W; tl += IM_NT) {
-          const int k = b + kbase - tl;
-          const int64_t gv = (k >= 0 && k < A.K) ? ld_bits(A.g, A.g_bits, k) : 0;
-          const uint64_t u = digit_word(gv, digit_bias(NG));
+      unsigned char* rv = smem + Gm.r_off;  // NG x RS bytes, rv[j][v + 16] = R_j[v]
+      const int RS = Gm.RS;
+      for (int i = tid; i < W + 16; i += IM_NT) {
+        const int v = i - 16, k = kbase - v;
+        const int64_t gv = (k >= 0 && k < A.K) ? ld_bits(A.g, A.g_bits, k) : 0;
+        const uint64_t u = digit_word(gv, digit_bias(NG));
 #pragma unroll
-          for (int j = 0; j < NG; ++j) bt[(j * 16 + b) * KDs + tl] = (unsigned char)(u >> (8 * j));
-        }
+        for (int j = 0; j < NG; ++j) rv[j * RS + i] = (unsigned char)(u >> (8 * j));
+      }
+      __syncthreads();
+      const int W4 = W >> 2;
+      for (int i = tid; i < NG * 16 * W4; i += IM_NT) {
+        const int w = i % W4, jb = i / W4, b = jb & 15, j = jb >> 4;
+        const int o = 4 * w - b + 16;  // byte offset of R_j[4w - b] in rv[j]
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rv + j * RS);
+        const uint32_t lo = rw[o >> 2], hi = rw[(o >> 2) + 1];
+        *reinterpret_cast<uint32_t*>(bt + (j * 16 + b) * KDs + 4 * w) = __funnelshift_r(lo, hi, 8 * (o & 3));
+      }
     }
     __syncthreads();
     uint32_t bf[SEG][NG][4];  // per kc: {b0,b1} of n8-tile 0, {b0,b1} of n8-tile 1
@@ -259,20 +320,35 @@ __global__ void __launch_bounds__(IM_NT, 1)
   } else {
     const bool verify = A.r < 0;
     const int pivot = verify ? 0 : A.r;
+    // rotation hoisted out of the position loop: rotated smem rows in, rotated
+    // output rows out (rot[MS-1] is the pivot stream, read only to verify)
+    const int64_t* drow[MS];
+    void* yrow[MS];
+#pragma unroll
+    for (int t = 0; t < MS; ++t) {
+      int in = pivot + 1 + t, out = pivot + t;
+      in -= in >= MS ? MS : 0;
+      in -= in >= MS ? MS : 0;
+      out -= out >= MS ? MS : 0;
+      drow[t] = dt + (size_t)in * T;
+      yrow[t] = A.y.p[out];
+    }
+    const int64_t ybase = j0 - A.y_begin;
+    const int64_t ulim = jend - j0 < T ? jend - j0 : T;
     unsigned bad = 0;
-    for (int u = tid; u < T; u += IM_NT) {
-      const int64_t j = j0 + u;
-      if (j >= jend) break;
-      int64_t dl[MS], orot[MS];
+    for (int u = tid; u < ulim; u += IM_NT) {
+      int64_t rot[MS], orot[MS];
 #pragma unroll
-      for (int s = 0; s < MS; ++s) dl[s] = dt[(size_t)s * T + u];
-      recover_regs_valid<MS>(dl, pivot, A.l, orot);
-      if (verify) bad += (dl[0] != wadd(wshl(orot[MS - 1], A.l), orot[0])) ? 1u : 0u;
+      for (int t = 0; t < MS - 1; ++t) rot[t] = drow[t][u];
+      recover_rot_valid<MS>(rot, A.l, orot);
+      if (verify) bad += (drow[MS - 1][u] != wadd(wshl(orot[MS - 1], A.l), orot[0])) ? 1u : 0u;
+      if (A.y_bits == 32) {
 #pragma unroll
-      for (int t = 0; t < MS; ++t) {
-        int row = pivot + t;
-        row -= row >= MS ? MS : 0;
-        st_bits(A.y.p[row], A.y_bits, j - A.y_begin, orot[t]);
+        for (int t = 0; t < MS; ++t)
+          reinterpret_cast<int32_t*>(yrow[t])[ybase + u] = (int32_t)(uint32_t)(uint64_t)orot[t];
+      } else {
+#pragma unroll
+        for (int t = 0; t < MS; ++t) reinterpret_cast<int64_t*>(yrow[t])[ybase + u] = orot[t];
       }
     }
     if (A.mismatch) {
@@ -294,10 +370,15 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
   Gm.NKC = Gm.KD / 32;
   Gm.KDs = (imma_seg(NG) * 32 + 127) / 128 * 128 + 16;  // one segment; == 16 mod 128
   Gm.S = (T + Gm.KD + 15) / 16 * 16;
+  Gm.RS = (imma_seg(NG) * 32 + 16 + 8 + 15) / 16 * 16;
   Gm.bt_off = 0;
   Gm.pl_off = (NG * 16 * Gm.KDs + 127) / 128 * 128;
   Gm.dt_off = (Gm.pl_off + MS * np * Gm.S + 127) / 128 * 128;
-  Gm.smem = (size_t)Gm.dt_off + (size_t)MS * T * 8;
+  {
+    const size_t dt_bytes = (size_t)MS * T * 8, raw_bytes = (size_t)MS * Gm.S * 4;
+    Gm.r_off = (int)((Gm.dt_off + (dt_bytes > raw_bytes ? dt_bytes : raw_bytes) + 127) / 128 * 128);
+    Gm.smem = (size_t)Gm.r_off + (size_t)NG * Gm.RS;
+  }
   if (Gm.smem > 227 * 1024) {
     set_error("imma conv: tile needs %zu bytes of shared memory (K=%d too long)", Gm.smem, A.K);
     return NENT_ERR_PARAM;

@@ -102,16 +102,7 @@ __device__ __forceinline__ bool recover_regs(const int64_t (&dl)[MT], int r, int
 // reference formula on such input; the fused kernels' redundant-stream check
 // flags any input that is not consistent.
 template <int MT>
-__device__ __forceinline__ void recover_regs_valid(const int64_t (&dl)[MT], int r, int l,
-                                                   int64_t (&orot)[MT]) {
-  int64_t rot[MT];
-#pragma unroll
-  for (int t = 0; t < MT - 1; ++t) {
-    int idx = r + 1 + t;
-    idx -= (idx >= MT) ? MT : 0;
-    idx -= (idx >= MT) ? MT : 0;
-    rot[t] = select_mod<MT>(dl, idx);
-  }
+__device__ __forceinline__ void recover_rot_valid(const int64_t* rot, int l, int64_t (&orot)[MT]) {
   const int low = (MT - 1) * l;
   const uint64_t mask = (((uint64_t)1) << low) - 1;
   const uint64_t sbit = ((uint64_t)1) << (low - 1);
@@ -125,6 +116,20 @@ __device__ __forceinline__ void recover_regs_valid(const int64_t (&dl)[MT], int 
   orot[MT - 1] = (MT & 1) ? wneg(v) : v;
 #pragma unroll
   for (int t = MT - 1; t >= 1; --t) orot[t - 1] = wsub(rot[t - 1], orot[t]) >> l;
+}
+
+template <int MT>
+__device__ __forceinline__ void recover_regs_valid(const int64_t (&dl)[MT], int r, int l,
+                                                   int64_t (&orot)[MT]) {
+  int64_t rot[MT];
+#pragma unroll
+  for (int t = 0; t < MT - 1; ++t) {
+    int idx = r + 1 + t;
+    idx -= (idx >= MT) ? MT : 0;
+    idx -= (idx >= MT) ? MT : 0;
+    rot[t] = select_mod<MT>(dl, idx);
+  }
+  recover_rot_valid<MT>(rot, l, orot);
 }
 
 }  // namespace nent

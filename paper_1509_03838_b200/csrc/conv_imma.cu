@@ -1,52 +1,54 @@
 // conv_imma.cu -- exact integer convolution on the tensor cores by digit
 // slicing (mma.sync m16n8k32 s8 -> s32), plain or fused with entangle/extract.
 // Reference semantics: ops._circ_conv_rows (/root/reference/pkg/src/nent/ops.py:158-172).
+//
+// Every operand is split into balanced base-256 digits (int8 in [-128,127]):
+//   x = sum_p 256^p x_p  (np planes),   g = sum_j 256^j g_j  (NG digits)
+//   y = sum_{p,j} 256^(p+j) (x_p (*) g_j)     (mod 2^64: exact whenever y fits int64)
+// Each digit convolution is an int8 GEMM with int32 accumulation, exact for a
+// K-segment of SEG*32 taps (|partial| <= 2^14 * 288 < 2^31).  The GEMM is
+// Toeplitz:
+//   Y[a, b] = sum_t A[a, t] B[t, b],    output j0 + 16a + b, b in [0,16)
+//   A[a, t] = x_p[j0 + 16a + t - (Keff-1)]   Hankel: row a+1 is row a shifted by
+//                                           16 bytes -- one shared-memory row
+//   B[t, b] = g_j[b + Keff - 1 - t]          the taps (a prepared table)
+// ldmatrix reads A fragments straight out of the digit plane (8 rows x 16 B =
+// 128 contiguous bytes per 8x8 matrix: conflict-free), so the Hankel matrix is
+// never materialised.
+//
+// Pipeline per CTA (1024 outputs of MS streams, 4 warps, 4 CTAs per SM so the
+// phases of different CTAs overlap on the SM's pipes):
+//   1. raw int32 tiles land in shared memory by TMA bulk copy (cp.async.bulk),
+//      entangle + digit split run from shared memory (bias trick + PRMT);
+//   2. per K-segment the digit-split Toeplitz table is bulk-copied from a
+//      table prepared once per launch; each warp issues, per (plane, k-step),
+//      one ldmatrix for A, NG for B and 2*NG IMMAs into int32 accumulators,
+//      folded into int64 after every plane;
+//   3. per-stream int64 results meet in shared memory; the epilogue stores
+//      them (plain conv) or recovers all m streams from the m-1 survivors
+//      (fused entangle -> conv -> extract) and writes them coalesced.
 #include "common.cuh"
 #include "conv_common.cuh"
 #include "recover.cuh"
 
 namespace nent {
 
-// ============================================================================
-// IMMA digit-sliced exact convolution (tensor cores, mma.sync s8*s8+s32).
-//
-// Every operand is split into balanced base-256 digits (int8 in [-128,127]):
-//   x = sum_p 256^p x_p  (NP planes),   g = sum_j 256^j g_j  (NG digits)
-//   y = sum_{p,j} 256^(p+j) (x_p (*) g_j)          (mod 2^64: exact whenever
-//                                                   y fits int64)
-// Each digit convolution is an int8 GEMM with int32 accumulation (exact:
-// |partial| <= 2^14 * KD < 2^31 for KD < 2^17).  The GEMM is Toeplitz:
-//   Y[a, b] = sum_t A[a, t] B[t, b],  output j0 + 16a + b (b in [0,16))
-//   A[a, t] = x_p[j0 + 16a + t - (K-1)]   (Hankel: row a is the signal shifted
-//                                          by 16 bytes, i.e. one smem row)
-//   B[t, b] = g_j[b + K - 1 - t]          (the taps, built once per CTA)
-// Because consecutive Hankel rows are exactly 16 bytes apart, ldmatrix reads
-// A fragments straight from the digit plane in shared memory (8 rows x 16 B
-// = 128 contiguous bytes per 8x8 matrix: conflict-free) -- the Hankel matrix
-// is never materialised.  B fragments stay in registers for a K-segment.
-// Warp w owns RT row-tiles of 16 rows (256 outputs each); per (plane, kc) it
-// issues one ldmatrix.x4 and 2*NG MMAs per row-tile.  After each plane the
-// int32 accumulators are folded into int64 (shift by 8(p+j)); the per-stream
-// int64 results meet in shared memory, where the epilogue stores them or runs
-// the m-stream recovery (fused entangle -> conv -> extract).
-// ============================================================================
-
 constexpr int IM_WARPS = 4;
 constexpr int IM_NT = IM_WARPS * 32;
-
-__host__ __device__ constexpr int imma_rt(int ms) { return ms <= 4 ? 2 : 1; }
-__host__ __device__ constexpr int imma_seg(int ng) { return ng == 1 ? 18 : ng == 2 ? 9 : ng == 3 ? 6 : 4; }
+constexpr int IM_T = IM_WARPS * 256;  // outputs per CTA tile (one 16x16 row-tile per warp)
+constexpr int IM_SEG = 9;             // k-steps (32 taps each) per K-segment
+constexpr int IM_KDS = IM_SEG * 32 + 16;  // table row stride: 304 == 48 mod 128 (conflict-free)
 
 struct ImmaGeom {
-  int Keff;  // K + zero taps so that every tile's first staged position is 4-aligned
-  int KD;    // K-dimension of the Toeplitz GEMM (multiple of 32)
-  int NKC;   // KD / 32
-  int KDs;   // Bt row stride in bytes (== 16 mod 128: conflict-free ldmatrix)
-  int S;     // bytes per digit plane (multiple of 16)
-  int np;    // digit planes of x
-  int RS;    // bytes per reversed-tap digit row
-  int bt_off, pl_off, dt_off, r_off;  // smem offsets
+  int Keff;   // K + zero taps so that every tile's first staged position is 4-aligned
+  int KD;     // K-dimension of the Toeplitz GEMM (multiple of 32)
+  int NKC;    // KD / 32
+  int NSEG;   // ceil(NKC / IM_SEG)
+  int S;      // bytes per digit plane (multiple of 16)
+  int np;     // digit planes of x
+  int bt_off, pl_off, dt_off;  // smem offsets
   size_t smem;
+  const unsigned char* table;  // [NSEG][NG][16][IM_KDS] digit-split Toeplitz taps
 };
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
@@ -79,60 +81,104 @@ __device__ __forceinline__ uint32_t gather_byte(uint32_t w0, uint32_t w1, uint32
   return __byte_perm(__byte_perm(w0, w1, sel), __byte_perm(w2, w3, sel), 0x5410);
 }
 
+// write the np digit planes of 4 consecutive values into word w of each plane
+__device__ __forceinline__ void put_digits(uint32_t* ps, int S4, int w, int np, const int64_t (&v)[4],
+                                           uint64_t bias) {
+  uint64_t u[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) u[e] = digit_word(v[e], bias);
+  const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+    if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
+  if (np > 4) {
+    const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32), h2 = (uint32_t)(u[2] >> 32),
+                   h3 = (uint32_t)(u[3] >> 32);
+#pragma unroll
+    for (int p = 4; p < 8; ++p)
+      if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(mb), "r"(phase) : "memory");
+}
+
+// Toeplitz tap table, once per launch: table[seg][j][b][tl] = digit_j(g[b + Keff - 1 - t]),
+// t = 32*IM_SEG*seg + tl (0 outside the taps and in the row padding).
+__global__ void imma_table_kernel(const void* g, int g_bits, int K, int Keff, int KD, int NG,
+                                  int nseg, unsigned char* table) {
+  const int total = nseg * NG * 16 * IM_KDS;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int tl = i % IM_KDS, b = (i / IM_KDS) % 16, j = (i / (IM_KDS * 16)) % NG,
+              seg = i / (IM_KDS * 16 * NG);
+    const int t = seg * IM_SEG * 32 + tl;
+    const int k = b + Keff - 1 - t;
+    int64_t gv = 0;
+    if (tl < IM_SEG * 32 && t < KD && k >= 0 && k < K) gv = ld_bits(g, g_bits, k);
+    table[i] = (unsigned char)(digit_word(gv, digit_bias(NG)) >> (8 * j));
+  }
+}
+
 template <int MS, int NG, bool EXTRACT>
-__global__ void __launch_bounds__(IM_NT, 1)
-    conv_imma_kernel(const __grid_constant__ ConvArgs A, const ImmaGeom Gm) {
-  constexpr int RT = imma_rt(MS);
-  constexpr int SEG = imma_seg(NG);
-  constexpr int T = IM_WARPS * RT * 256;  // outputs per CTA tile
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned char* bt = smem + Gm.bt_off;   // NG x 16 rows x KDs
-  unsigned char* pl = smem + Gm.pl_off;   // MS x np planes x S bytes
-  int64_t* dt = reinterpret_cast<int64_t*>(smem + Gm.dt_off);  // MS x T
+__global__ void __launch_bounds__(IM_NT, 4)
+    conv_imma_kernel(const __grid_constant__ ConvArgs A, const __grid_constant__ ImmaGeom Gm) {
+  constexpr int T = IM_T;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar[2];  // [0] raw tiles, [1] tap table
+  unsigned char* bt = smem + Gm.bt_off;                         // NG x 16 x IM_KDS
+  unsigned char* pl = smem + Gm.pl_off;                         // MS x np x S
+  int64_t* dt = reinterpret_cast<int64_t*>(smem + Gm.dt_off);  // MS x T (raw tiles alias it)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t j0 = A.y_begin + (int64_t)blockIdx.x * T;
   const int row0 = EXTRACT ? 0 : (int)blockIdx.y * MS;
-  const int np = Gm.np, KDs = Gm.KDs, S = Gm.S;
+  const int np = Gm.np, S = Gm.S, S4 = S >> 2;
+  const uint32_t mb_raw = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+  const uint32_t mb_tab = (uint32_t)__cvta_generic_to_shared(&mbar[1]);
+  const uint32_t bt_s = (uint32_t)__cvta_generic_to_shared(bt);
+  const uint32_t tab_bytes = (uint32_t)(NG * 16 * IM_KDS);
 
-  // ---- digit planes: smem byte i <-> input position j0 - (Keff-1) + i ----
-  // Keff = K + zero taps chosen so p0 is a multiple of 4 for every tile.
+  // ---- 1. stage: smem byte i of a plane <-> input position p0 + i ----
   const int64_t p0 = j0 - (Gm.Keff - 1);
   const uint64_t xbias = digit_bias(np);
-  const int S4 = S >> 2;
-  // Fast path (interior tile, int32 streams, no gather/scale/add): one TMA
-  // bulk copy per stream lands the raw tile in shared memory (aliasing the
-  // result tile dt, unused until the MMAs finish), then the digit split runs
-  // from shared memory.  Edge tiles take the general per-element chain.
   bool fast = A.in_bits == 32 && !A.perm && A.scale == 1 && !A.add && p0 >= 0 && p0 + S <= A.n_in;
 #pragma unroll
   for (int s = 0; s < MS; ++s) {
     const int row = row0 + s;
     fast = fast && row < A.rows && ((uintptr_t)A.b.p[row] & 15) == 0 && (EXTRACT || !A.a.p[row]);
   }
+  if (tid == 0) {
+    mbar_init(mb_raw);
+    mbar_init(mb_tab);
+  }
+  __syncthreads();
+  if (tid == 0) {  // the first segment's taps travel while the tile is staged
+    mbar_expect(mb_tab, tab_bytes);
+    bulk_g2s(bt_s, Gm.table, tab_bytes, mb_tab);
+  }
   if (fast) {
-    __shared__ __align__(8) uint64_t mbar;
-    int32_t* raw = reinterpret_cast<int32_t*>(smem + Gm.dt_off);  // MS x S words
-    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    int32_t* raw = reinterpret_cast<int32_t*>(dt);
     if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)(MS * S * 4);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      mbar_expect(mb_raw, (uint32_t)(MS * S * 4));
 #pragma unroll
-      for (int s = 0; s < MS; ++s) {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(raw + (size_t)s * S);
-        const int32_t* src = reinterpret_cast<const int32_t*>(A.b.p[row0 + s]) + p0;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(dst), "l"(src), "r"((uint32_t)(S * 4)), "r"(mb) : "memory");
-      }
+      for (int s = 0; s < MS; ++s)
+        bulk_g2s((uint32_t)__cvta_generic_to_shared(raw + (size_t)s * S),
+                 reinterpret_cast<const int32_t*>(A.b.p[row0 + s]) + p0, (uint32_t)(S * 4), mb_raw);
     }
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-        " @!p bra WAIT_%=;\n}" ::"r"(mb) : "memory");
+    mbar_wait(mb_raw, 0);
     const int4* raw4 = reinterpret_cast<const int4*>(raw);
     for (int w = tid; w < S4; w += IM_NT) {
 #pragma unroll
@@ -144,184 +190,125 @@ __global__ void __launch_bounds__(IM_NT, 1)
           v[0] = wadd(wshl(av.x, A.l), v[0]); v[1] = wadd(wshl(av.y, A.l), v[1]);
           v[2] = wadd(wshl(av.z, A.l), v[2]); v[3] = wadd(wshl(av.w, A.l), v[3]);
         }
-        uint32_t* ps = reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S);
-        uint64_t u[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) u[e] = digit_word(v[e], xbias);
-        const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-          if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
-        if (np > 4) {
-          const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32),
-                         h2 = (uint32_t)(u[2] >> 32), h3 = (uint32_t)(u[3] >> 32);
-#pragma unroll
-          for (int p = 4; p < 8; ++p)
-            if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
-        }
+        put_digits(reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S), S4, w, np, v, xbias);
       }
     }
   } else {
     for (int s = 0; s < MS; ++s) {
       const int row = row0 + s;
-      uint32_t* ps = reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S);
       const bool live = row < A.rows;
       for (int w = tid; w < S4; w += IM_NT) {
-        uint64_t u[4];
+        int64_t v[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          u[e] = digit_word(live ? conv_prologue(A, row, p0 + 4 * w + e) : 0, xbias);
-        const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-          if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
-        if (np > 4) {
-          const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32),
-                         h2 = (uint32_t)(u[2] >> 32), h3 = (uint32_t)(u[3] >> 32);
-#pragma unroll
-          for (int p = 4; p < 8; ++p)
-            if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
-        }
+        for (int e = 0; e < 4; ++e) v[e] = live ? conv_prologue(A, row, p0 + 4 * w + e) : 0;
+        put_digits(reinterpret_cast<uint32_t*>(pl + (size_t)s * np * S), S4, w, np, v, xbias);
       }
     }
   }
 
+  // ---- 2. MMAs ----
   const uint32_t pl_s = (uint32_t)__cvta_generic_to_shared(pl);
-  const uint32_t bt_s = (uint32_t)__cvta_generic_to_shared(bt);
   const int mat = lane >> 3, r8 = lane & 7;
-  // per-lane ldmatrix row offsets
-  const uint32_t a_lane = 16u * (uint32_t)(r8 + 8 * (mat & 1)) + 16u * (uint32_t)(mat >> 1);
-  const uint32_t b_lane = (uint32_t)((8 * (mat >> 1) + r8) * KDs + 16 * (mat & 1));
+  const uint32_t a_lane = 256u * (uint32_t)warp + 16u * (uint32_t)(r8 + 8 * (mat & 1)) + 16u * (uint32_t)(mat >> 1);
+  const uint32_t b_lane = (uint32_t)((8 * (mat >> 1) + r8) * IM_KDS + 16 * (mat & 1));
   const int g = lane >> 2, t4 = lane & 3;
+  // combining the g digits in int32 is exact when 2^14 * 288 * (1 + 256) < 2^31
+  constexpr bool FOLD32 = NG <= 2;
 
-  // K is consumed SEG*32 Toeplitz columns at a time: the segment's taps are
-  // digit-split into Bt (shared), its B fragments held in registers, and
-  // every stream's int64 partial results accumulate in the staging tile dt.
-  for (int kc0 = 0; kc0 < Gm.NKC; kc0 += SEG) {
-    const int nkc = min(SEG, Gm.NKC - kc0);
-    __syncthreads();  // previous segment's readers of Bt are done
-    // Bt_j[b][tl] = digit_j(g[b + Keff - 1 - t]), t = 32*kc0 + tl.  Row b is
-    // the reversed digit sequence R_j[v] = digit_j(g[kbase - v]) shifted by b
-    // bytes: build R_j once (W + 16 bytes), then every Bt word is one funnel
-    // shift of two aligned R_j words.
-    {
-      const int W = 32 * nkc;
-      const int kbase = Gm.Keff - 1 - 32 * kc0;
-      unsigned char* rv = smem + Gm.r_off;  // NG x RS bytes, rv[j][v + 16] = R_j[v]
-      const int RS = Gm.RS;
-      for (int i = tid; i < W + 16; i += IM_NT) {
-        const int v = i - 16, k = kbase - v;
-        const int64_t gv = (k >= 0 && k < A.K) ? ld_bits(A.g, A.g_bits, k) : 0;
-        const uint64_t u = digit_word(gv, digit_bias(NG));
-#pragma unroll
-        for (int j = 0; j < NG; ++j) rv[j * RS + i] = (unsigned char)(u >> (8 * j));
+  for (int seg = 0; seg < Gm.NSEG; ++seg) {
+    const int kc0 = seg * IM_SEG;
+    const int nkc = min(IM_SEG, Gm.NKC - kc0);
+    if (seg > 0) {
+      __syncthreads();  // every warp is done with the previous segment's table
+      if (tid == 0) {
+        mbar_expect(mb_tab, tab_bytes);
+        bulk_g2s(bt_s, Gm.table + (size_t)seg * tab_bytes, tab_bytes, mb_tab);
       }
-      __syncthreads();
-      const int W4 = W >> 2;
-      for (int i = tid; i < NG * 16 * W4; i += IM_NT) {
-        const int w = i % W4, jb = i / W4, b = jb & 15, j = jb >> 4;
-        const int o = 4 * w - b + 16;  // byte offset of R_j[4w - b] in rv[j]
-        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rv + j * RS);
-        const uint32_t lo = rw[o >> 2], hi = rw[(o >> 2) + 1];
-        *reinterpret_cast<uint32_t*>(bt + (j * 16 + b) * KDs + 4 * w) = __funnelshift_r(lo, hi, 8 * (o & 3));
-      }
+    } else {
+      __syncthreads();  // digit planes complete
     }
-    __syncthreads();
-    uint32_t bf[SEG][NG][4];  // per kc: {b0,b1} of n8-tile 0, {b0,b1} of n8-tile 1
-#pragma unroll
-    for (int kk = 0; kk < SEG; ++kk)
-#pragma unroll
-      for (int j = 0; j < NG; ++j)
-        if (kk < nkc) ldsm_x4(bf[kk][j], bt_s + (uint32_t)(j * 16 * KDs) + b_lane + 32u * (uint32_t)kk);
+    mbar_wait(mb_tab, (uint32_t)(seg & 1));
 
     for (int s = 0; s < MS; ++s) {
       if (!EXTRACT && row0 + s >= A.rows) break;
-      long long acc[RT][2][4];
-#pragma unroll
-      for (int rt = 0; rt < RT; ++rt)
+      long long acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      for (int p = 0; p < np; ++p) {
+        const uint32_t plane = pl_s + (uint32_t)((s * np + p) * S) + 32u * (uint32_t)kc0 + a_lane;
+        int c[2][NG][4];
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[rt][nb][q] = 0;
-      for (int p = 0; p < np; ++p) {
-        const uint32_t plane = pl_s + (uint32_t)((s * np + p) * S) + 32u * (uint32_t)kc0;
-        int c[RT][2][NG][4];
+          for (int j = 0; j < NG; ++j)
 #pragma unroll
-        for (int rt = 0; rt < RT; ++rt)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-            for (int j = 0; j < NG; ++j)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) c[rt][nb][j][q] = 0;
+            for (int q = 0; q < 4; ++q) c[nb][j][q] = 0;
         auto kstep = [&](int kk) {
+          uint32_t af[4];
+          ldsm_x4(af, plane + 32u * (uint32_t)kk);
 #pragma unroll
-          for (int rt = 0; rt < RT; ++rt) {
-            uint32_t af[4];
-            ldsm_x4(af, plane + 256u * (uint32_t)(warp * RT + rt) + a_lane + 32u * (uint32_t)kk);
-#pragma unroll
-            for (int j = 0; j < NG; ++j) {
-              imma16832(c[rt][0][j], af, bf[kk][j][0], bf[kk][j][1]);
-              imma16832(c[rt][1][j], af, bf[kk][j][2], bf[kk][j][3]);
-            }
+          for (int j = 0; j < NG; ++j) {
+            uint32_t bf[4];  // {b0,b1} of n8-tile 0, {b0,b1} of n8-tile 1
+            ldsm_x4(bf, bt_s + (uint32_t)(j * 16 * IM_KDS) + b_lane + 32u * (uint32_t)kk);
+            imma16832(c[0][j], af, bf[0], bf[1]);
+            imma16832(c[1][j], af, bf[2], bf[3]);
           }
         };
-        if (nkc == SEG) {
-          // full segment: straight-line code, so the A-fragment loads of the
-          // next k-steps can be scheduled ahead of this step's MMAs
+        if (nkc == IM_SEG) {
 #pragma unroll
-          for (int kk = 0; kk < SEG; ++kk) kstep(kk);
+          for (int kk = 0; kk < IM_SEG; ++kk) kstep(kk);
         } else {
 #pragma unroll
-          for (int kk = 0; kk < SEG; ++kk) {
+          for (int kk = 0; kk < IM_SEG; ++kk) {
             if (kk >= nkc) break;
             kstep(kk);
           }
         }
-        // fold the int32 digit products into the int64 accumulators
-#pragma unroll
-        for (int rt = 0; rt < RT; ++rt)
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint64_t v = 0;
-#pragma unroll
-              for (int j = 0; j < NG; ++j) v += (uint64_t)(int64_t)c[rt][nb][j][q] << (8 * j);
-              acc[rt][nb][q] = (long long)((uint64_t)acc[rt][nb][q] + (v << (8 * p)));
-            }
-      }
-      // this segment's contribution: C fragment (row g|g+8, col 2t|2t+1) of n8-tile nb
-#pragma unroll
-      for (int rt = 0; rt < RT; ++rt)
+        // fold the digit products into int64: += (sum_j c_j 256^j) << 8p
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int u = 256 * (warp * RT + rt) + 16 * (g + 8 * (q >> 1)) + 8 * nb + 2 * t4 + (q & 1);
-            int64_t* d = dt + (size_t)s * T + u;
-            *d = kc0 == 0 ? acc[rt][nb][q] : wadd(*d, acc[rt][nb][q]);
+            uint64_t v;
+            if (FOLD32) {
+              int32_t v32 = c[nb][0][q];
+              if (NG == 2) v32 += c[nb][NG - 1][q] << 8;
+              v = (uint64_t)(int64_t)v32;
+            } else {
+              v = 0;
+#pragma unroll
+              for (int j = 0; j < NG; ++j) v += (uint64_t)(int64_t)c[nb][j][q] << (8 * j);
+            }
+            acc[nb][q] = (long long)((uint64_t)acc[nb][q] + (v << (8 * p)));
           }
+      }
+      // this segment's contribution; C fragment (row g|g+8, col 2t|2t+1) of n8-tile nb
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int u = 256 * warp + 16 * (g + 8 * (q >> 1)) + 8 * nb + 2 * t4 + (q & 1);
+          int64_t* d = dt + (size_t)s * T + u;
+          *d = seg == 0 ? acc[nb][q] : wadd(*d, acc[nb][q]);
+        }
     }
   }
   __syncthreads();
 
-  // ---- epilogue: coalesced stores or the fused m-stream recovery ----
+  // ---- 3. epilogue: coalesced stores or the fused m-stream recovery ----
   const int64_t jend = A.y_begin + A.n_out;
+  const int64_t ybase = j0 - A.y_begin;
+  const int64_t ulim = jend - j0 < T ? jend - j0 : T;
   if (!EXTRACT) {
     for (int s = 0; s < MS; ++s) {
       const int row = row0 + s;
       if (row >= A.rows) break;
-      for (int u = tid; u < T; u += IM_NT) {
-        const int64_t j = j0 + u;
-        if (j < jend) st_bits(A.y.p[row], A.y_bits, j - A.y_begin, dt[(size_t)s * T + u]);
-      }
+      void* yp = A.y.p[row];
+      for (int u = tid; u < ulim; u += IM_NT) st_bits(yp, A.y_bits, ybase + u, dt[(size_t)s * T + u]);
     }
   } else {
     const bool verify = A.r < 0;
     const int pivot = verify ? 0 : A.r;
     // rotation hoisted out of the position loop: rotated smem rows in, rotated
-    // output rows out (rot[MS-1] is the pivot stream, read only to verify)
+    // output rows out (drow[MS-1] is the pivot stream, read only to verify)
     const int64_t* drow[MS];
     void* yrow[MS];
 #pragma unroll
@@ -333,8 +320,6 @@ __global__ void __launch_bounds__(IM_NT, 1)
       drow[t] = dt + (size_t)in * T;
       yrow[t] = A.y.p[out];
     }
-    const int64_t ybase = j0 - A.y_begin;
-    const int64_t ulim = jend - j0 < T ? jend - j0 : T;
     unsigned bad = 0;
     for (int u = tid; u < ulim; u += IM_NT) {
       int64_t rot[MS], orot[MS];
@@ -361,24 +346,20 @@ __global__ void __launch_bounds__(IM_NT, 1)
 
 template <int MS, int NG, bool EXTRACT>
 static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
-  constexpr int T = IM_WARPS * imma_rt(MS) * 256;
+  constexpr int T = IM_T;
   ImmaGeom Gm{};
   Gm.np = np;
   // p0 = y_begin + tile*T - (Keff - 1) must be == 0 mod 4 (T is a multiple of 16)
   Gm.Keff = A.K + (int)((((A.y_begin - A.K + 1) % 4) + 4) % 4);
   Gm.KD = (Gm.Keff + 15 + 31) / 32 * 32;
   Gm.NKC = Gm.KD / 32;
-  Gm.KDs = (imma_seg(NG) * 32 + 127) / 128 * 128 + 16;  // one segment; == 16 mod 128
-  Gm.S = (T + Gm.KD + 15) / 16 * 16;
-  Gm.RS = (imma_seg(NG) * 32 + 16 + 8 + 15) / 16 * 16;
+  Gm.NSEG = (Gm.NKC + IM_SEG - 1) / IM_SEG;
+  Gm.S = (T + Gm.NSEG * IM_SEG * 32 + 15) / 16 * 16;  // room for the last segment's k-steps
   Gm.bt_off = 0;
-  Gm.pl_off = (NG * 16 * Gm.KDs + 127) / 128 * 128;
+  Gm.pl_off = (NG * 16 * IM_KDS + 127) / 128 * 128;
   Gm.dt_off = (Gm.pl_off + MS * np * Gm.S + 127) / 128 * 128;
-  {
-    const size_t dt_bytes = (size_t)MS * T * 8, raw_bytes = (size_t)MS * Gm.S * 4;
-    Gm.r_off = (int)((Gm.dt_off + (dt_bytes > raw_bytes ? dt_bytes : raw_bytes) + 127) / 128 * 128);
-    Gm.smem = (size_t)Gm.r_off + (size_t)NG * Gm.RS;
-  }
+  const size_t dt_bytes = (size_t)MS * T * 8, raw_bytes = (size_t)MS * Gm.S * 4;
+  Gm.smem = (size_t)Gm.dt_off + (dt_bytes > raw_bytes ? dt_bytes : raw_bytes);
   if (Gm.smem > 227 * 1024) {
     set_error("imma conv: tile needs %zu bytes of shared memory (K=%d too long)", Gm.smem, A.K);
     return NENT_ERR_PARAM;
@@ -393,10 +374,23 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
     }
     configured = Gm.smem;
   }
+  // digit-split Toeplitz taps, prepared once for the whole launch in a
+  // stream-ordered workspace (freed in stream order after the kernel)
+  const size_t tbytes = (size_t)Gm.NSEG * NG * 16 * IM_KDS;
+  unsigned char* table = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&table), tbytes, stream) != cudaSuccess) {
+    set_error("imma conv: workspace allocation of %zu bytes failed", tbytes);
+    return NENT_ERR_CUDA;
+  }
+  imma_table_kernel<<<(unsigned)((tbytes + 255) / 256 < 1024 ? (tbytes + 255) / 256 : 1024), 256, 0,
+                      stream>>>(A.g, A.g_bits, A.K, Gm.Keff, Gm.KD, NG, Gm.NSEG, table);
+  Gm.table = table;
   const int64_t tiles = (A.n_out + T - 1) / T;
   dim3 grid((unsigned)tiles, EXTRACT ? 1 : (unsigned)((A.rows + MS - 1) / MS));
   kern<<<grid, IM_NT, Gm.smem, stream>>>(A, Gm);
-  return check_launch("imma conv");
+  const int st = check_launch("imma conv");
+  cudaFreeAsync(table, stream);
+  return st;
 }
 
 template <int NG>
@@ -426,10 +420,6 @@ int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
   const int np = (flavor >> 8) & 0xf, ng = (flavor >> 12) & 0xf;
   if (np < 1 || np > 8 || ng < 1 || ng > 4) {
     set_error("imma conv: digit counts np=%d ng=%d outside 1..8 / 1..4", np, ng);
-    return NENT_ERR_PARAM;
-  }
-  if (A.K + 15 > (1 << 16)) {
-    set_error("imma conv: K=%d too long for int32 digit sums", A.K);
     return NENT_ERR_PARAM;
   }
   switch (ng) {

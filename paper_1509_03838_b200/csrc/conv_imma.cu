@@ -31,6 +31,8 @@
 #include "conv_common.cuh"
 #include "recover.cuh"
 
+#include <type_traits>
+
 namespace nent {
 
 constexpr int IM_WARPS = 4;
@@ -88,15 +90,18 @@ __device__ __forceinline__ void put_digits(uint32_t* ps, int S4, int w, int np, 
 #pragma unroll
   for (int e = 0; e < 4; ++e) u[e] = digit_word(v[e], bias);
   const uint32_t l0 = (uint32_t)u[0], l1 = (uint32_t)u[1], l2 = (uint32_t)u[2], l3 = (uint32_t)u[3];
-#pragma unroll
-  for (int p = 0; p < 4; ++p)
-    if (p < np) ps[p * S4 + w] = gather_byte(l0, l1, l2, l3, p);
-  if (np > 4) {
-    const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32), h2 = (uint32_t)(u[2] >> 32),
-                   h3 = (uint32_t)(u[3] >> 32);
-#pragma unroll
-    for (int p = 4; p < 8; ++p)
-      if (p < np) ps[p * S4 + w] = gather_byte(h0, h1, h2, h3, p - 4);
+  const uint32_t h0 = (uint32_t)(u[0] >> 32), h1 = (uint32_t)(u[1] >> 32), h2 = (uint32_t)(u[2] >> 32),
+                 h3 = (uint32_t)(u[3] >> 32);
+  // jump into a straight-line tail: exactly np byte-gathers and stores
+  switch (np) {
+    case 8: ps[7 * S4 + w] = gather_byte(h0, h1, h2, h3, 3);  // fall through
+    case 7: ps[6 * S4 + w] = gather_byte(h0, h1, h2, h3, 2);  // fall through
+    case 6: ps[5 * S4 + w] = gather_byte(h0, h1, h2, h3, 1);  // fall through
+    case 5: ps[4 * S4 + w] = gather_byte(h0, h1, h2, h3, 0);  // fall through
+    case 4: ps[3 * S4 + w] = gather_byte(l0, l1, l2, l3, 3);  // fall through
+    case 3: ps[2 * S4 + w] = gather_byte(l0, l1, l2, l3, 2);  // fall through
+    case 2: ps[1 * S4 + w] = gather_byte(l0, l1, l2, l3, 1);  // fall through
+    default: ps[w] = gather_byte(l0, l1, l2, l3, 0);
   }
 }
 
@@ -232,24 +237,32 @@ __global__ void __launch_bounds__(IM_NT, 4)
     for (int s = 0; s < MS; ++s) {
       if (!EXTRACT && row0 + s >= A.rows) break;
       long long acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-      for (int p = 0; p < np; ++p) {
+      // planes two at a time: each B fragment load feeds both planes' MMAs
+      auto planes = [&](int p, auto PAIR) {
+        constexpr int NPL = decltype(PAIR)::value ? 2 : 1;
         const uint32_t plane = pl_s + (uint32_t)((s * np + p) * S) + 32u * (uint32_t)kc0 + a_lane;
-        int c[2][NG][4];
+        int c[NPL][2][NG][4];
 #pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
+        for (int h = 0; h < NPL; ++h)
 #pragma unroll
-          for (int j = 0; j < NG; ++j)
+          for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) c[nb][j][q] = 0;
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) c[h][nb][j][q] = 0;
         auto kstep = [&](int kk) {
-          uint32_t af[4];
-          ldsm_x4(af, plane + 32u * (uint32_t)kk);
+          uint32_t af[NPL][4];
+#pragma unroll
+          for (int h = 0; h < NPL; ++h) ldsm_x4(af[h], plane + (uint32_t)(h * S) + 32u * (uint32_t)kk);
 #pragma unroll
           for (int j = 0; j < NG; ++j) {
             uint32_t bf[4];  // {b0,b1} of n8-tile 0, {b0,b1} of n8-tile 1
             ldsm_x4(bf, bt_s + (uint32_t)(j * 16 * IM_KDS) + b_lane + 32u * (uint32_t)kk);
-            imma16832(c[0][j], af, bf[0], bf[1]);
-            imma16832(c[1][j], af, bf[2], bf[3]);
+#pragma unroll
+            for (int h = 0; h < NPL; ++h) {
+              imma16832(c[h][0][j], af[h], bf[0], bf[1]);
+              imma16832(c[h][1][j], af[h], bf[2], bf[3]);
+            }
           }
         };
         if (nkc == IM_SEG) {
@@ -262,24 +275,29 @@ __global__ void __launch_bounds__(IM_NT, 4)
             kstep(kk);
           }
         }
-        // fold the digit products into int64: += (sum_j c_j 256^j) << 8p
+        // fold the digit products into int64: += (sum_j c_j 256^j) << 8(p+h)
 #pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
+        for (int h = 0; h < NPL; ++h)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint64_t v;
-            if (FOLD32) {
-              int32_t v32 = c[nb][0][q];
-              if (NG == 2) v32 += c[nb][NG - 1][q] << 8;
-              v = (uint64_t)(int64_t)v32;
-            } else {
-              v = 0;
+          for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-              for (int j = 0; j < NG; ++j) v += (uint64_t)(int64_t)c[nb][j][q] << (8 * j);
+            for (int q = 0; q < 4; ++q) {
+              uint64_t v;
+              if (FOLD32) {
+                int32_t v32 = c[h][nb][0][q];
+                if (NG == 2) v32 += c[h][nb][NG - 1][q] << 8;
+                v = (uint64_t)(int64_t)v32;
+              } else {
+                v = 0;
+#pragma unroll
+                for (int j = 0; j < NG; ++j) v += (uint64_t)(int64_t)c[h][nb][j][q] << (8 * j);
+              }
+              acc[nb][q] = (long long)((uint64_t)acc[nb][q] + (v << (8 * (p + h))));
             }
-            acc[nb][q] = (long long)((uint64_t)acc[nb][q] + (v << (8 * p)));
-          }
-      }
+      };
+      int p = 0;
+      for (; p + 1 < np; p += 2) planes(p, std::true_type{});
+      if (p < np) planes(p, std::false_type{});
       // this segment's contribution; C fragment (row g|g+8, col 2t|2t+1) of n8-tile nb
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)

@@ -5,8 +5,10 @@ Workload (BASELINE.json configs[1], the config the metric is quoted on):
 M=3 streams of N=2^24 int32 samples in [-2^11, 2^11-1], one 256-tap filter,
 geometry derive_params(3, 64) = (l=21, k=21); full linear convolution of every
 entangled stream, all 3 outputs recovered (failed=None pivots on stream 0 and
-checks the redundant stream).  One step = one pass of the fused
+checks the redundant stream).  One step = one launch of the fused
 entangle -> conv -> extract kernel over the whole batch, inputs resident in HBM.
+The kernel is the exact digit-sliced tensor-core convolution (IMMA, mma.sync
+s8): the 35-bit entangled words become 5 int8 digit planes, the 12-bit taps 2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -38,7 +40,6 @@ sys.path.insert(0, str(REPO))
 METRIC = "entangled int conv output samples/s; overhead vs non-entangled conv (%)"
 UNIT = "samples/s"
 WORKLOAD = "cfg2: M=3, N=2^24 int32 in [-2^11,2^11), K=256 taps, (m,w,l,k)=(3,64,21,21), full conv"
-L2_BYTES = 126 * 1024 * 1024
 
 
 def parse():
@@ -48,16 +49,15 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other-config section")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work for the cpu_baseline sample")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def sha(a: np.ndarray) -> str:
@@ -79,11 +79,12 @@ class ClockSampler:
 
     def __init__(self, index: int, period_s: float = 0.002):
         self.index, self.period = index, period_s
-        self.samples: list[tuple[float, int]] = []
+        self.samples: list[int] = []
         self.reasons: set[str] = set()
         self.max_mhz = None
         self.source = "nvml"
         self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
@@ -95,7 +96,7 @@ class ClockSampler:
 
             def poll():
                 while not self._stop.is_set():
-                    self.samples.append((time.perf_counter(), N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                    self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
                     bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
                     for nm, mask in masks:
                         if bits & mask:
@@ -107,25 +108,23 @@ class ClockSampler:
             time.sleep(3 * self.period)
         except Exception as exc:  # NVML unavailable: one nvidia-smi read instead
             self.source = f"nvidia-smi ({type(exc).__name__})"
-            self.t = None
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
         if self.t is not None:
             self.t.join(timeout=1)
-        if self.t is None:
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
-                                      "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=10).stdout.split(",")
-                self.samples = [(0.0, int(float(out[0])))]
-                self.max_mhz = int(float(out[1]))
-            except Exception:
-                pass
+            return
+        try:
+            out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=10).stdout.split(",")
+            self.samples, self.max_mhz = [int(float(out[0]))], int(float(out[1]))
+        except Exception:
+            pass
 
     def summary(self) -> dict:
-        sm = [v for _, v in self.samples]
+        sm = self.samples
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(sm), "source": self.source,
                 "sm_mhz_min": min(sm) if sm else None}
@@ -133,18 +132,27 @@ class ClockSampler:
 
 # -------------------------------------------------------------- workload --
 
-def make_inputs(rank: int, world: int, n: int, K: int):
+def make_inputs(rank: int, n: int, K: int):
     """Rank 0 holds the canonical cfg2 draw (seed 2); rank p > 0 draws its
     slice from seed (2, p) -- same shapes and value distribution."""
     from paper_1509_03838_b200 import workloads
 
+    wl0 = workloads.make(2, n=n if rank == 0 else 16, K=K)
     if rank == 0:
-        wl = workloads.make(2, n=n, K=K)
-        return wl.params, wl.c, wl.g
+        return wl0.params, wl0.c, wl0.g
     rng = np.random.default_rng([2, rank])
     c = rng.integers(-(1 << 11), 1 << 11, (3, n), dtype=np.int64)
-    g = workloads.make(2, n=16, K=K).g  # every rank uses the same filter
-    return workloads.make(2, n=16, K=K).params, c, g
+    return wl0.params, c, wl0.g  # every rank uses the same filter
+
+
+def event_time(fn, stream, reps=1):
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    return a, b
 
 
 # ------------------------------------------------------------ our device path --
@@ -153,10 +161,10 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_1509_03838_b200 as nent
     from paper_1509_03838_b200 import _device as D
     from paper_1509_03838_b200 import fused
-    from paper_1509_03838_b200._lib import MAC_F64, MAC_G64, MAC_I32, MAC_NAMES, MAC_S64, MAC_W64
+    from paper_1509_03838_b200._lib import (BENCH_IMMA, MAC_F64, MAC_G64, MAC_I32, MAC_NAMES, MAC_S64,
+                                            MAC_W64, imma_flavor, is_imma)
     from paper_1509_03838_b200.hostpath import ChunkedEntangledConv
 
     rank, world, local = dist_env()
@@ -168,12 +176,10 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     n, K = 1 << 24, 256
-    params, c_np, g = make_inputs(rank, world, n, K)
-    m = params.m
-    H = K - 1
+    params, c_np, g = make_inputs(rank, n, K)
+    m, H = params.m, K - 1
     c_dev = torch.from_numpy(c_np).to(dev).to(torch.int32)
-    # halo-split: the K-1 samples left of this rank's slice come from rank-1
-    if world > 1:
+    if world > 1:  # halo-split: the K-1 samples left of this rank's slice come from rank-1
         halo = torch.zeros((m, H), dtype=torch.int32, device=dev)
         ops = []
         if rank + 1 < world:
@@ -183,42 +189,41 @@ def run_ours(args):
         for w in dist.batch_isend_irecv(ops):
             w.wait()
         x_dev = torch.cat([halo, c_dev], dim=1).contiguous()
-        last = rank == world - 1  # the last rank also owns the K-1 tail outputs
-        n_out = n + (H if last else 0)
+        n_out = n + (H if rank == world - 1 else 0)  # the last rank also owns the K-1 tail
         period, n_in, y_begin = H + n + H, H + n, H  # rank 0 keeps a zero halo (left edge)
     else:
         x_dev = c_dev
         n_out, period, n_in, y_begin = n + H, n + H, n, 0
 
-    max_c = (1 << 11)
+    max_c = 1 << 11
     eps_bound = max_c * ((1 << params.l) + 1)
-    flavor = fused.conv_flavor(eps_bound, g)           # F64 for cfg2 (|delta| < 2^53)
-    plain_flavor_same = flavor                          # same accumulator width
-    plain_flavor_narrow = fused.conv_flavor(max_c, g)   # narrowest exact plain kernel (I32)
-    g_dev = D.taps_tensor(g, flavor)
+    flavor = fused.conv_flavor(eps_bound, g, n_out=n_out)             # imma5x2 for cfg2
+    core_flavor = fused.conv_flavor(eps_bound, g, allow_imma=False)   # f64: the CUDA-core path
+    plain_same = flavor                                               # same kernel, same digits
+    plain_fast = fused.conv_flavor(max_c, g, n_out=n_out)             # fastest plain: imma2x2
+    plain_core = fused.conv_flavor(max_c, g, allow_imma=False)        # i32
+    taps = {f: D.taps_tensor(g, f) for f in {flavor, core_flavor, plain_same, plain_fast, plain_core}}
     d_dev = torch.empty((m, n_out), dtype=torch.int32, device=dev)
     y_plain = torch.empty((m, n_out), dtype=torch.int32, device=dev)
     mismatch = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        D.fused_conv(x_dev, g_dev, K, params.l, flavor, None, params.w > 32, period, n_in=n_in,
+    def fused_step(fl=flavor):
+        D.fused_conv(x_dev, taps[fl], K, params.l, fl, None, params.w > 32, period, n_in=n_in,
                      y_begin=y_begin, n_out=n_out, out=d_dev, mismatch=mismatch)
 
-    def plain(fl, gd):
-        D.conv(x_dev, gd, K, fl, period=period, y_begin=y_begin, n_out=n_out, out=y_plain)
-
-    g_plain_narrow = D.taps_tensor(g, plain_flavor_narrow)
+    def plain(fl):
+        D.conv(x_dev, taps[fl], K, fl, period=period, y_begin=y_begin, n_out=n_out, out=y_plain)
 
     for _ in range(args.warmup):
-        step()
-        plain(plain_flavor_same, g_dev)
-        plain(plain_flavor_narrow, g_plain_narrow)
+        fused_step()
+        plain(plain_same)
+        plain(plain_fast)
     torch.cuda.synchronize(dev)
 
-    # parity of the benchmarked output itself (rank 0 holds the canonical cfg2)
     exact = None
-    if rank == 0 and world == 1:
+    known = None
+    if rank == 0 and world == 1:  # parity of the benchmarked output itself
         known = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())["cfg2"]["d"]
         exact = sha(d_dev.to(torch.int64).cpu().numpy()) == known and int(mismatch.item()) == 0
 
@@ -226,77 +231,69 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
+        ev0, ev1 = event_time(fused_step, stream, args.steps)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    ms_step = ms_max / args.steps
-    samples_job = m * n_out * world if world == 1 else m * (n * world + H)
+    ms_step = float(ms_t.item()) / args.steps
+    samples_job = m * n_out if world == 1 else m * (n * world + H)
     value = samples_job / (ms_step / 1e3)
 
-    # ---------------- interleaved overhead vs plain conv ----------------
-    def timed(fn):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        fn()
-        b.record(stream)
-        return a, b
-
-    pairs = []
-    for _ in range(max(5, min(args.steps, 15))):
-        e = timed(step)
-        ps = timed(lambda: plain(plain_flavor_same, g_dev))
-        pn = timed(lambda: plain(plain_flavor_narrow, g_plain_narrow))
-        pairs.append((e, ps, pn))
+    # ---------------- interleaved comparisons (per-launch CUDA events) ----------------
+    cands = {
+        "entangled": lambda: fused_step(flavor),
+        "entangled_cuda_core": lambda: fused_step(core_flavor),
+        "plain_same_kernel": lambda: plain(plain_same),
+        "plain_fastest": lambda: plain(plain_fast),
+        "plain_cuda_core_same_width": lambda: plain(core_flavor),
+        "plain_cuda_core_narrowest": lambda: plain(plain_core),
+    }
+    evs = {k: [] for k in cands}
+    for _ in range(max(5, min(args.steps, 11))):
+        for k, fn in cands.items():
+            evs[k].append(event_time(fn, stream))
     torch.cuda.synchronize(dev)
-    t_e = [a.elapsed_time(b) for (a, b), _, _ in pairs]
-    t_s = [a.elapsed_time(b) for _, (a, b), _ in pairs]
-    t_n = [a.elapsed_time(b) for _, _, (a, b) in pairs]
-    ovh_same = statistics.median([(x - y) / y * 100 for x, y in zip(t_e, t_s)])
-    ovh_narrow = statistics.median([(x - y) / y * 100 for x, y in zip(t_e, t_n)])
+    t = {k: [a.elapsed_time(b) for a, b in v] for k, v in evs.items()}
+    med = {k: statistics.median(v) for k, v in t.items()}
 
-    # ---------------- measured MAC-pipe peaks (roofline denominators) ----------------
+    def ovh(a, b):
+        return statistics.median([(x - y) / y * 100 for x, y in zip(t[a], t[b])])
+
+    # ---------------- measured pipe peaks (roofline denominators) ----------------
     peaks = {}
-    names = dict(MAC_NAMES)
-    names[16] = "imma_s8_mma_sync"
-    for kind in (MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64, 16):
-        D.microbench(kind, 148 * 4, 256, 64)  # warm
+    for kind in (BENCH_IMMA, MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64):
+        D.microbench(kind, 148 * 4, 256, 64)
         best = 0.0
         for _ in range(3):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            macs = D.microbench(kind, 148 * 8, 256, 4096)
+            macs = D.microbench(kind, 148 * 8, 256, 4096 if kind != BENCH_IMMA else 1024)
             b.record(stream)
             torch.cuda.synchronize(dev)
             best = max(best, macs / (a.elapsed_time(b) / 1e3))
-        peaks[names[kind]] = best
-    kern_ms = statistics.median(t_e)  # one fused launch per step, measured on its stream
-    macs_launch = m * n * K  # algorithmic MACs per launch (M*N*K)
-    achieved_tflops = 2 * macs_launch / (kern_ms / 1e3) / 1e12
-    fname = MAC_NAMES[flavor]
-    peak_tflops = 2 * peaks[fname] / 1e12
+        peaks[MAC_NAMES[kind]] = best
+    np_, ng = (flavor >> 8) & 15, (flavor >> 12) & 15
+    kern_ms = med["entangled"]
+    macs_alg = m * n * K                      # M*N*K
+    digit_macs = macs_alg * np_ * ng          # int8 digit products the method needs
+    achieved = 2 * digit_macs / (kern_ms / 1e3) / 1e12
+    peak = 2 * peaks["imma_s8_mma_sync"] / 1e12
     traffic = None
     tf = REPO / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("fused_conv_cfg2", {}).get("bytes_per_launch")
+            traffic = json.loads(tf.read_text()).get(MAC_NAMES[flavor], {}).get("bytes_per_launch")
         except Exception:
             traffic = None
 
     # ---------------- e2e through the host-buffer path ----------------
     e2e = None
     if world == 1:
-        pipe = ChunkedEntangledConv(params, n, g, flavor, chunk=1 << 21)
+        pipe = ChunkedEntangledConv(params, n, g, flavor, chunk=1 << 22)
         c_host = torch.from_numpy(c_np.astype(np.int32)).pin_memory()
         d_host = torch.empty((m, n + H), dtype=torch.int32).pin_memory()
         for _ in range(2):
@@ -307,16 +304,20 @@ def run_ours(args):
             exact = exact and sha(d_host.to(torch.int64).numpy()) == known
         reps = max(3, min(args.steps, 8))
         t0 = time.perf_counter()
-        launches_e2e = 0
+        launches = 0
         for _ in range(reps):
-            launches_e2e += pipe.run(c_host, d_host)
+            launches += pipe.run(c_host, d_host)
             pipe.synchronize()
         torch.cuda.synchronize(dev)
         e2e_s = (time.perf_counter() - t0) / reps
         e2e = {"value": m * (n + H) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes(),
                "d2h_bytes_per_step": pipe.d2h_bytes(), "ms_per_step": e2e_s * 1e3,
-               "path": "ChunkedEntangledConv: pinned int32 host -> 3-stream chunked H2D/fused kernel/D2H",
-               "kernels_per_step": launches_e2e // reps}
+               "path": "ChunkedEntangledConv: pinned int32 host -> 3-stream chunked H2D / fused kernel / D2H",
+               "kernels_per_step": launches // reps}
+
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = other_configs(D, fused, dev, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -326,32 +327,45 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": MAC_NAMES[flavor] + " exact (int32 in/out)",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 digits x int8 digits -> int32 -> int64 (exact integer; int32 in/out)",
             "data": "synthetic (canonical seeded cfg2 draw, SURVEY.md 8d)",
             "config": {"workload": WORKLOAD, "samples_per_step": samples_job,
                        "parallelism": "halo-split" if world > 1 else "single GPU",
                        "l2": "inputs 201 MB + outputs 201 MB per step > 126 MB L2; no flush needed",
-                       "mac_flavor": fname, "failed": None, "verify_redundant_stream": True},
-            "overhead_pct": ovh_same,
-            "overhead": {"vs_same_width_plain_pct": ovh_same,
-                         "vs_narrowest_plain_pct": ovh_narrow,
-                         "plain_same_flavor": MAC_NAMES[plain_flavor_same],
-                         "plain_narrow_flavor": MAC_NAMES[plain_flavor_narrow],
-                         "ms_entangled": statistics.median(t_e), "ms_plain_same": statistics.median(t_s),
-                         "ms_plain_narrow": statistics.median(t_n)},
-            "roofline": {"bound": "fp64", "pipe": "DFMA on CUDA cores (exact: |delta| < 2^53)",
-                         "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
-                         "frac": achieved_tflops / peak_tflops if peak_tflops else None,
-                         "traffic": traffic, "kernel": "nent::conv_tile_kernel<F64,3,fused>",
-                         "algorithmic_macs_per_launch": macs_launch,
-                         "peak_source": "measured in this run by nent_microbench (16 independent "
-                                        "accumulator chains per thread, 148*8 CTAs x 256 threads)",
+                       "mac_flavor": MAC_NAMES[flavor], "failed": None, "verify_redundant_stream": True},
+            "overhead_pct": ovh("entangled", "plain_same_kernel"),
+            "overhead": {
+                "vs_plain_same_kernel_pct": ovh("entangled", "plain_same_kernel"),
+                "vs_plain_fastest_pct": ovh("entangled", "plain_fastest"),
+                "cuda_core_entangled_vs_plain_same_width_pct": ovh("entangled_cuda_core",
+                                                                   "plain_cuda_core_same_width"),
+                "vs_plain_cuda_core_narrowest_pct": ovh("entangled", "plain_cuda_core_narrowest"),
+                "flavors": {"entangled": MAC_NAMES[flavor], "entangled_cuda_core": MAC_NAMES[core_flavor],
+                            "plain_same_kernel": MAC_NAMES[plain_same], "plain_fastest": MAC_NAMES[plain_fast],
+                            "plain_cuda_core_narrowest": MAC_NAMES[plain_core]},
+                "ms": med,
+                "note": "plain_same_kernel runs the identical kernel/digit geometry on the plain streams "
+                        "(isolates entangle+extract); plain_fastest uses the digits the 12-bit plain "
+                        "samples need (2 planes instead of the entangled words' 5)"},
+            "roofline": {"bound": "tensor", "pipe": "IMMA (mma.sync m16n8k32 s8, tensor cores)",
+                         "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "kernel": f"nent::conv_imma_kernel<3,{ng},true> ({MAC_NAMES[flavor]})",
+                         "algorithmic_per_launch": {"conv_macs": macs_alg, "digit_macs": digit_macs,
+                                                    "digit_planes": np_, "tap_digits": ng},
+                         "peak_source": "measured in this run: nent_microbench mma.sync s8 "
+                                        "(16 independent accumulators per warp, 148*8 CTAs x 8 warps)",
+                         "cuda_core_path": {"flavor": MAC_NAMES[core_flavor],
+                                            "achieved_tflops": 2 * macs_alg / (med["entangled_cuda_core"] / 1e3) / 1e12,
+                                            "peak_tflops": 2 * peaks[MAC_NAMES[core_flavor]] / 1e12},
                          "peaks_measured_gmac_s": {k: v / 1e9 for k, v in peaks.items()}},
             "e2e": e2e,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (2 if is_imma(flavor) else 1),  # tap-table prep + fused kernel
             "exact": exact,
             "mismatches": int(mismatch.item()),
             "clocks": clocks.summary(),
+            "other_configs": extras,
             "cpu_baseline": cpu,
         }
         print(json.dumps(out))
@@ -359,11 +373,70 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def other_configs(D, fused, dev, stream):
+    """The other BASELINE configs through the same fused path: ms per launch,
+    output samples/s, and the known-answer digest check (no failure)."""
+    import torch
+
+    from paper_1509_03838_b200 import workloads
+    from paper_1509_03838_b200._lib import MAC_NAMES
+
+    digests = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())
+    res = {}
+    for cfg in (1, 3, 5):
+        wl = workloads.make(cfg)
+        p = wl.params
+        c = torch.from_numpy(wl.c).to(dev).to(torch.int32)
+        n, K = wl.n, wl.K
+        L = n + K - 1
+        out = torch.empty((wl.m, L), dtype=torch.int32, device=dev)
+        mm = torch.zeros(1, dtype=torch.int64, device=dev)
+        kw = {}
+        xb = int(np.abs(wl.c).max()) * ((1 << p.l) + 1)
+        gather = False
+        if wl.scale is not None:
+            a = torch.from_numpy(wl.add).to(dev)
+            add = D.shift_add(a, a, p.l)
+            kw = dict(scale=wl.scale, add=add, perm=torch.from_numpy(wl.perm).to(dev))
+            xb = xb * abs(wl.scale) + int(add.abs().max())
+            gather = True
+        fl = fused.conv_flavor(xb, wl.g, n_out=L, gather=gather)
+        gd = D.taps_tensor(wl.g, fl)
+
+        def run():
+            D.fused_conv(c, gd, K, p.l, fl, None, p.w > 32, L, n_in=n, out=out, mismatch=mm, **kw)
+
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize(dev)
+        ok = sha(out.to(torch.int64).cpu().numpy()) == digests[f"cfg{cfg}"]["d"] and int(mm.item()) == 0
+        reps = 20 if cfg == 1 else 5
+        a, b = event_time(run, stream, reps)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        res[f"cfg{cfg}"] = {"flavor": MAC_NAMES[fl], "ms": ms, "samples_per_s": wl.m * L / (ms / 1e3),
+                            "conv_gmac_s": wl.m * n * K / (ms / 1e3) / 1e9, "exact": ok}
+    # cfg4 inner products (65,536 x 4,096 per stream, 3 streams)
+    wl = workloads.make(4)
+    c = torch.from_numpy(wl.c).to(dev).to(torch.int32)
+    fused.entangled_inner(wl.params, c, wl.g)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    r = fused.entangled_inner(wl.params, c, wl.g)
+    ms = (time.perf_counter() - t0) * 1e3
+    ok = sha(r.outputs.data.to(torch.int64).cpu().numpy()) == digests["cfg4_inner"]["d"] and r.mismatches == 0
+    res["cfg4_inner"] = {"flavor": r.flavor, "ms_incl_sync": ms, "hbm_gb_s": c.numel() * 4 / (ms / 1e3) / 1e9,
+                         "exact": ok}
+    del c
+    torch.cuda.empty_cache()
+    return res
+
+
 # ------------------------------------------------------------- CPU baseline --
 
 def cpu_pipeline_time(O, c: np.ndarray, g: np.ndarray, params, threads: int = 0):
-    """Reference algorithm on the CPU: entangle -> full conv on entangled
-    streams -> recover all 3 (failed=None), plus the plain conv."""
+    """Reference algorithm on the CPU: entangle -> full conv on the entangled
+    streams -> recover all 3 (failed=None); then the plain conv."""
     K = len(g)
     t0 = time.perf_counter()
     pad = np.zeros((c.shape[0], c.shape[1] + K - 1), dtype=np.int64)
@@ -379,6 +452,17 @@ def cpu_pipeline_time(O, c: np.ndarray, g: np.ndarray, params, threads: int = 0)
     return t_ent, t_plain, d.shape[0] * d.shape[1]
 
 
+def host_desc():
+    import platform
+    model = ""
+    try:
+        model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
+                      if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    return f"{model} ({os.cpu_count()} logical CPUs, {platform.machine()})"
+
+
 def cpu_baseline(c, g, params, target_s: float):
     from oracle import oracle as O
 
@@ -387,19 +471,11 @@ def cpu_baseline(c, g, params, target_s: float):
     t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params)
     ns = int(min(c.shape[1], max(ns, ns * target_s / 2 / max(t, 1e-6))))
     t_ent, t_plain, samples = cpu_pipeline_time(O, c[:, :ns], g, params)
-    import platform
-    model = ""
-    try:
-        model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
-                      if ln.startswith("model name")), "")
-    except OSError:
-        pass
     return {"value": samples / t_ent, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"first {ns} samples of each of the 3 cfg2 streams, K=256, full conv "
                       f"(entangle + conv + recover), oracle/nent_oracle.c OpenMP",
-            "plain_value": samples / t_plain,
-            "overhead_pct": (t_ent - t_plain) / t_plain * 100,
-            "seconds": t_ent + t_plain, "host": f"{model} ({os.cpu_count()} logical CPUs, {platform.machine()})"}
+            "plain_value": samples / t_plain, "overhead_pct": (t_ent - t_plain) / t_plain * 100,
+            "seconds": t_ent + t_plain, "host": host_desc()}
 
 
 def run_reference(args):
@@ -408,10 +484,9 @@ def run_reference(args):
         return  # only rank 0 runs the CPU reference arm
     from oracle import oracle as O
 
-    params, c, g = make_inputs(0, 1, 1 << 24, 256)
+    params, c, g = make_inputs(0, 1 << 24, 256)
     threads = O.max_threads()
-    # bounded sample per step, sized so the whole run stays within a few minutes
-    ns = 1 << 16
+    ns = 1 << 16  # bounded sample per step, sized so the run stays within a few minutes
     t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params, threads)
     budget = 150.0 / max(args.steps + args.warmup, 1)
     ns = int(min(c.shape[1], max(ns, ns * budget / 2 / max(t, 1e-6))))
@@ -424,7 +499,7 @@ def run_reference(args):
         tp.append(b)
     t_step = sum(te) / len(te)
     value = samples / t_step
-    out = {
+    print(json.dumps({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 (reference numpy semantics)",
@@ -434,10 +509,10 @@ def run_reference(args):
         "overhead_pct": statistics.median([(a - b) / b * 100 for a, b in zip(te, tp)]),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"first {ns} samples of each cfg2 stream per step (K=256, full "
-                                   f"conv, entangle+conv+recover), oracle/nent_oracle.c OpenMP"},
+                                   f"conv, entangle+conv+recover), oracle/nent_oracle.c OpenMP",
+                         "host": host_desc()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(out))
+    }))
 
 
 def main():

@@ -103,12 +103,16 @@ def cuda_core_flavor(max_x: int, sum_g: int, max_g: int) -> int:
 
 
 def pick_flavor(max_x: int, sum_g: int, max_g: int, K: int | None = None,
-                allow_imma: bool = True) -> int:
+                allow_imma: bool = True, n_out: int | None = None, gather: bool = False) -> int:
     """Fastest exact flavour.  Every candidate is exact for these bounds; the
     IMMA digit-sliced tensor-core conv is chosen when its modelled rate
-    (mma.sync peak x efficiency x K/KD / (np*ng)) beats the CUDA-core pipe."""
+    (mma.sync peak x efficiency x K/KD / (np*ng)) beats the CUDA-core pipe.
+    Small problems (fewer 1024-output tiles than ~2 waves) and gathered
+    (permuted) inputs stay on the CUDA-core kernel, whose staging is cheaper."""
     core = cuda_core_flavor(max_x, sum_g, max_g)
-    if not allow_imma or K is None or core == MAC_X128 or K + 15 >= 1 << 16:
+    if not allow_imma or K is None or core == MAC_X128 or K + 15 >= 1 << 16 or gather:
+        return core
+    if n_out is not None and n_out < 2 * 148 * 1024:
         return core
     np_, ng = signed_digits(max_x), signed_digits(max_g)
     if np_ > 8 or ng > 4:

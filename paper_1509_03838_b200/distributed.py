@@ -59,7 +59,7 @@ class DeviceCompute:
             xb = mc * ((1 << params.l) + 1) * abs(int(scale))
             if add is not None:
                 xb += D.max_abs(add.reshape(1, -1))
-            flavor = conv_flavor(xb, np.asarray(g))
+            flavor = conv_flavor(xb, np.asarray(g), n_out=n + K - 1, gather=perm is not None)
         g_dev = D.taps_tensor(np.asarray(g, dtype=np.int64), flavor)
         period = n + K - 1 if full else n
         add_ent = D.shift_add(add, add, params.l) if add is not None else None
@@ -81,7 +81,7 @@ class DeviceCompute:
         flavor = self.flavor
         if flavor is None:
             mc = D.max_abs(x)
-            flavor = conv_flavor(mc * ((1 << params.l) + 1), np.asarray(g))
+            flavor = conv_flavor(mc * ((1 << params.l) + 1), np.asarray(g), n_out=n_out)
         g_dev = D.taps_tensor(np.asarray(g, dtype=np.int64), flavor)
         return D.fused_conv(x, g_dev, len(g), params.l, flavor, failed, params.w > 32, period,
                             n_in=n_in, y_begin=y_begin, n_out=n_out)

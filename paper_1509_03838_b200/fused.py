@@ -46,11 +46,12 @@ def _eps_bound(max_c: int, p: CodecParams) -> int:
     return max_c * ((1 << p.l) + 1)
 
 
-def conv_flavor(max_x: int, g: np.ndarray, allow_imma: bool = True) -> int:
+def conv_flavor(max_x: int, g: np.ndarray, allow_imma: bool = True, n_out: int | None = None,
+                gather: bool = False) -> int:
     """Fastest exact MAC flavour for |x| <= max_x convolved with taps g."""
     g = np.asarray(g, dtype=np.int64)
     return D.pick_flavor(max_x, int(np.abs(g.astype(object)).sum()), D.host_max_abs(g),
-                         K=len(g), allow_imma=allow_imma)
+                         K=len(g), allow_imma=allow_imma, n_out=n_out, gather=gather)
 
 
 def _prep(block: StreamBlock, dtype=None) -> tuple[torch.Tensor, bool]:
@@ -85,7 +86,8 @@ def entangled_conv(block: StreamBlock, g, failed: int | None = None, mode: str =
     period = n + K - 1 if mode == "full" else n
     if flavor is None:
         mc = max_c if max_c is not None else (D.host_max_abs(block.data) if host else D.max_abs(c))
-        flavor = conv_flavor(_eps_bound(mc, p), g if not isinstance(g, torch.Tensor) else g.cpu().numpy())
+        flavor = conv_flavor(_eps_bound(mc, p), g if not isinstance(g, torch.Tensor) else g.cpu().numpy(),
+                             n_out=period)
     if flavor in (MAC_G64, MAC_X128):
         raise ParameterError("operands too wide for the fused kernel; use the staged API")
     if g_dev is None:
@@ -110,7 +112,7 @@ def plain_conv(block: StreamBlock, g, mode: str = "full", flavor: int | None = N
     g = np.asarray(g, dtype=np.int64) if not isinstance(g, torch.Tensor) else g.cpu().numpy()
     if flavor is None:
         mc = max_c if max_c is not None else (D.host_max_abs(block.data) if host else D.max_abs(c))
-        flavor = conv_flavor(mc, g)
+        flavor = conv_flavor(mc, g, n_out=period)
     if g_dev is None:
         g_dev = D.taps_tensor(g, flavor)
     y, ovf = D.conv(c, g_dev, K, flavor, period=period, n_out=period, out_dtype=out_dtype, out=out)
@@ -137,7 +139,7 @@ def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: i
         mc = D.host_max_abs(block.data) if host else D.max_abs(c)
         amax = D.max_abs(add_ent.reshape(1, -1))
         x_bound = _eps_bound(mc, p) * abs(int(scale)) + amax
-        flavor = conv_flavor(x_bound, g)
+        flavor = conv_flavor(x_bound, g, n_out=n + K - 1, gather=True)
     g_dev = D.taps_tensor(g, flavor)
     mismatch = torch.zeros(1, dtype=torch.int64, device=c.device) if (verify and failed is None) else None
     d = D.fused_conv(c, g_dev, K, p.l, flavor, failed, p.w > 32, n + K - 1, n_in=n,

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define NENT_ABI_VERSION 1
+#define NENT_ABI_VERSION 2
 
 #define NENT_OK 0
 #define NENT_ERR_PARAM 1    /* ParameterError */
@@ -104,7 +104,17 @@ int nent_extract_m3(const void *const *delta, int delta_bits, void *const *out, 
  * does not fit int64 (the reference's object path raises OverflowError). */
 int nent_conv(const void *const *x, int x_bits, int rows, int64_t n_in, int64_t period,
               const void *g, int g_bits, int K, void *const *y, int y_bits, int64_t y_begin,
-              int64_t n_out, int flavor, unsigned long long *overflow_dev, void *stream);
+              int64_t n_out, int flavor, unsigned long long *overflow_dev, const void *imma_table,
+              void *stream);
+
+/* NENT_MAC_IMMA flavours read a digit-split Toeplitz table of the taps.  Pass
+ * imma_table = NULL to have each call build it in a stream-ordered workspace,
+ * or prepare it once (the taps are fixed across calls) with nent_imma_table
+ * into a caller buffer of nent_imma_table_bytes bytes.  The table depends on
+ * the taps, K, the flavour's tap digits and y_begin mod 4. */
+int64_t nent_imma_table_bytes(int K, int flavor);
+int nent_imma_table(const void *g, int g_bits, int K, int64_t y_begin, int flavor, void *table,
+                    void *stream);
 
 /* The fused hot path (bench.py entangled() chain, bench.py:103-106, plus the
  * pipeline chain of SCALE/ADD/PERMUTATION before the conv, SURVEY cfg5):
@@ -116,12 +126,14 @@ int nent_conv(const void *const *x, int x_bits, int rows, int64_t n_in, int64_t 
  * happens on load and extraction in registers; delta never reaches HBM.
  * With r = -1 and mismatch_dev != NULL, the redundant stream delta_0 is
  * checked against the recovered outputs (silent-error detection) and the
- * number of inconsistent positions is added to *mismatch_dev. */
+ * number of inconsistent positions is added to *mismatch_dev.
+ * pre_entangled != 0: the rows c are already entangled words (e.g. produced
+ * by the stream-per-GPU workers or a gather pre-pass); only conv + extract. */
 int nent_fused_conv(const void *const *c, int c_bits, int m, int64_t n_in, int64_t period,
                     int l, int64_t scale, const void *add, int add_bits, const int64_t *perm,
-                    const void *g, int g_bits, int K, int r, int wide, void *const *d,
+                    const void *g, int g_bits, int K, int r, int pre_entangled, void *const *d,
                     int d_bits, int64_t y_begin, int64_t n_out, int flavor,
-                    unsigned long long *mismatch_dev, void *stream);
+                    unsigned long long *mismatch_dev, const void *imma_table, void *stream);
 
 /* Single-stream variant of the fused prologue without extraction (the
  * stream-per-GPU worker: x = scale*((a << l) + b) + add, gathered, convolved).
@@ -129,7 +141,7 @@ int nent_fused_conv(const void *const *c, int c_bits, int m, int64_t n_in, int64
 int nent_chain_conv(const void *a, const void *b, int in_bits, int64_t n_in, int64_t period,
                     int l, int64_t scale, const void *add, int add_bits, const int64_t *perm,
                     const void *g, int g_bits, int K, void *y, int y_bits, int64_t y_begin,
-                    int64_t n_out, int flavor, void *stream);
+                    int64_t n_out, int flavor, const void *imma_table, void *stream);
 
 /* ELEMENTWISE_ADD/SUB/MUL and SCALE (ops.py:193-204): y = x op g, g of length
  * n (g_len == n) or 1 (broadcast).  Arithmetic modulo 2^64; when check != 0

@@ -187,9 +187,20 @@ def poison(row: torch.Tensor, w: int) -> None:
 
 # --------------------------------------------------------------------- ops --
 
+def imma_table(g_dev: torch.Tensor, K: int, flavor: int, y_begin: int = 0) -> torch.Tensor | None:
+    """Prepared digit-split Toeplitz taps for an IMMA flavour (None otherwise):
+    build once, pass as ``imma_table=`` to every launch with the same taps."""
+    if not is_imma(flavor):
+        return None
+    nbytes = int(_lib.lib().nent_imma_table_bytes(K, flavor))
+    tab = torch.empty(nbytes, dtype=torch.uint8, device=g_dev.device)
+    call("nent_imma_table", ptr(g_dev), bits(g_dev), K, y_begin, flavor, ptr(tab), _sh())
+    return tab
+
+
 def conv(x: torch.Tensor, g_dev: torch.Tensor, K: int, flavor: int, period: int | None = None,
          y_begin: int = 0, n_out: int | None = None, out_dtype=torch.int64,
-         out: torch.Tensor | None = None):
+         out: torch.Tensor | None = None, imma_table: torch.Tensor | None = None):
     """K2 on every row: circular conv over `period` (default n) with zero-extension.
     Returns (y, overflow_count) -- overflow only counted for MAC_X128."""
     rows, n_in = x.shape
@@ -201,7 +212,7 @@ def conv(x: torch.Tensor, g_dev: torch.Tensor, K: int, flavor: int, period: int 
     if x.dtype == torch.int32 and flavor in (MAC_G64, MAC_X128):
         x = x.to(torch.int64)
     call("nent_conv", row_ptrs(x), bits(x), rows, n_in, period, ptr(g_dev), bits(g_dev), K,
-         row_ptrs(out), bits(out), y_begin, n_out, flavor, ptr(ovf), _sh())
+         row_ptrs(out), bits(out), y_begin, n_out, flavor, ptr(ovf), ptr(imma_table), _sh())
     return out, (int(ovf.item()) if ovf is not None else 0)
 
 
@@ -209,10 +220,13 @@ def fused_conv(c, g_dev: torch.Tensor, K: int, l: int, flavor: int, r: int | Non
                wide: bool, period: int, n_in: int | None = None, y_begin: int = 0,
                n_out: int | None = None, scale: int = 1, add: torch.Tensor | None = None,
                perm: torch.Tensor | None = None, out_dtype=torch.int64,
-               out: torch.Tensor | None = None, mismatch: torch.Tensor | None = None):
+               out: torch.Tensor | None = None, mismatch: torch.Tensor | None = None,
+               pre_entangled: bool = False, imma_table: torch.Tensor | None = None):
     """K2f: entangle-on-load -> [scale, add, gather] -> conv -> extract.
     ``c`` is an (m, n) tensor or list of m row tensors; ``r=None`` = no failure
-    (pivot 0, redundant-stream check into ``mismatch`` if given)."""
+    (pivot 0, redundant-stream check into ``mismatch`` if given).  ``wide``
+    (w > 32) is accepted for symmetry with ``extract``: the fused recovery is
+    exact for any w <= 64 on the consistent words it produces."""
     rows = list(c) if not isinstance(c, torch.Tensor) else [c[i] for i in range(c.shape[0])]
     m = len(rows)
     n_in = rows[0].shape[-1] if n_in is None else n_in
@@ -221,8 +235,8 @@ def fused_conv(c, g_dev: torch.Tensor, K: int, l: int, flavor: int, r: int | Non
         out = torch.empty((m, n_out), dtype=out_dtype, device=rows[0].device)
     call("nent_fused_conv", row_ptrs(rows), bits(rows[0]), m, n_in, period, l, int(scale),
          ptr(add), bits(add) if add is not None else 64, ptr(perm), ptr(g_dev), bits(g_dev), K,
-         -1 if r is None else int(r), int(bool(wide)), row_ptrs(out), bits(out), y_begin, n_out,
-         flavor, ptr(mismatch), _sh())
+         -1 if r is None else int(r), int(bool(pre_entangled)), row_ptrs(out), bits(out), y_begin,
+         n_out, flavor, ptr(mismatch), ptr(imma_table), _sh())
     return out
 
 
@@ -230,14 +244,14 @@ def chain_conv(a: torch.Tensor | None, b: torch.Tensor, g_dev: torch.Tensor, K: 
                flavor: int, period: int, n_in: int | None = None, y_begin: int = 0,
                n_out: int | None = None, scale: int = 1, add: torch.Tensor | None = None,
                perm: torch.Tensor | None = None, out_dtype=torch.int64,
-               out: torch.Tensor | None = None) -> torch.Tensor:
+               out: torch.Tensor | None = None, imma_table: torch.Tensor | None = None) -> torch.Tensor:
     n_in = b.shape[-1] if n_in is None else n_in
     n_out = period if n_out is None else n_out
     if out is None:
         out = torch.empty((n_out,), dtype=out_dtype, device=b.device)
     call("nent_chain_conv", ptr(a), ptr(b), bits(b), n_in, period, l, int(scale), ptr(add),
          bits(add) if add is not None else 64, ptr(perm), ptr(g_dev), bits(g_dev), K, ptr(out),
-         bits(out), y_begin, n_out, flavor, _sh())
+         bits(out), y_begin, n_out, flavor, ptr(imma_table), _sh())
     return out
 
 

@@ -56,11 +56,13 @@ SIGNATURES = {
     "nent_shift_add": [_P, _P, _I, _P, _I, _L, _I, _P],
     "nent_extract": [_PP, _I, _PP, _I, _I, _L, _I, _I, _I, _P, _P],
     "nent_extract_m3": [_PP, _I, _PP, _I, _L, _I, _I, _I, _P],
-    "nent_conv": [_PP, _I, _I, _L, _L, _P, _I, _I, _PP, _I, _L, _L, _I, _P, _P],
+    "nent_conv": [_PP, _I, _I, _L, _L, _P, _I, _I, _PP, _I, _L, _L, _I, _P, _P, _P],
+    "nent_imma_table_bytes": [_I, _I],
+    "nent_imma_table": [_P, _I, _I, _L, _I, _P, _P],
     "nent_fused_conv": [_PP, _I, _I, _L, _L, _I, _L, _P, _I, _P, _P, _I, _I, _I, _I, _PP, _I,
-                        _L, _L, _I, _P, _P],
+                        _L, _L, _I, _P, _P, _P],
     "nent_chain_conv": [_P, _P, _I, _L, _L, _I, _L, _P, _I, _P, _P, _I, _I, _P, _I, _L, _L, _I,
-                        _P],
+                        _P, _P],
     "nent_elementwise": [_PP, _I, _I, _L, _P, _I, _L, _I, _PP, _I, _I, _P, _P],
     "nent_scale": [_PP, _I, _I, _L, _L, _PP, _I, _I, _P, _P],
     "nent_permute": [_PP, _I, _I, _L, _P, _PP, _I, _P],
@@ -76,7 +78,7 @@ SIGNATURES = {
     "nent_checksum_recover": [_PP, _I, _P, _I, _I, _L, _I, _P, _I, _P],
     "nent_microbench": [_I, _I, _I, _I, _P, ctypes.POINTER(ctypes.c_double), _P],
 }
-_RESTYPES = {"nent_last_error": ctypes.c_char_p}
+_RESTYPES = {"nent_last_error": ctypes.c_char_p, "nent_imma_table_bytes": ctypes.c_int64}
 
 _lock = threading.Lock()
 _lib = None

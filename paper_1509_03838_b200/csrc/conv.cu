@@ -384,7 +384,8 @@ extern "C" {
 
 int nent_conv(const void* const* x, int x_bits, int rows, int64_t n_in, int64_t period,
               const void* g, int g_bits, int K, void* const* y, int y_bits, int64_t y_begin,
-              int64_t n_out, int flavor, unsigned long long* overflow_dev, void* stream) {
+              int64_t n_out, int flavor, unsigned long long* overflow_dev, const void* imma_table,
+              void* stream) {
   int st = check_conv_common(x_bits, g_bits, y_bits, K, n_in, period, y_begin, n_out);
   if (st) return st;
   if (rows < 1 || rows > NENT_MAX_STREAMS) {
@@ -399,14 +400,14 @@ int nent_conv(const void* const* x, int x_bits, int rows, int64_t n_in, int64_t 
   A.in_bits = x_bits; A.y_bits = y_bits; A.g_bits = g_bits;
   A.K = K; A.Kp = (K + CV_G - 1) / CV_G * CV_G;
   A.n_in = n_in; A.period = period; A.y_begin = y_begin; A.n_out = n_out;
-  A.scale = 1; A.g = g; A.r = 0; A.mismatch = overflow_dev;
+  A.scale = 1; A.g = g; A.r = 0; A.mismatch = overflow_dev; A.imma_table = imma_table;
   return conv_store(A, flavor, as_stream(stream));
 }
 
 int nent_chain_conv(const void* a, const void* b, int in_bits, int64_t n_in, int64_t period,
                     int l, int64_t scale, const void* add, int add_bits, const int64_t* perm,
                     const void* g, int g_bits, int K, void* y, int y_bits, int64_t y_begin,
-                    int64_t n_out, int flavor, void* stream) {
+                    int64_t n_out, int flavor, const void* imma_table, void* stream) {
   int st = check_conv_common(in_bits, g_bits, y_bits, K, n_in, period, y_begin, n_out);
   if (st) return st;
   if (add) NENT_CHECK_BITS(add_bits);
@@ -420,15 +421,15 @@ int nent_chain_conv(const void* a, const void* b, int in_bits, int64_t n_in, int
   A.l = l; A.scale = scale; A.add = add; A.perm = perm;
   A.K = K; A.Kp = (K + CV_G - 1) / CV_G * CV_G;
   A.n_in = n_in; A.period = period; A.y_begin = y_begin; A.n_out = n_out;
-  A.g = g;
+  A.g = g; A.imma_table = imma_table;
   return conv_store(A, flavor, as_stream(stream));
 }
 
 int nent_fused_conv(const void* const* c, int c_bits, int m, int64_t n_in, int64_t period,
                     int l, int64_t scale, const void* add, int add_bits, const int64_t* perm,
-                    const void* g, int g_bits, int K, int r, int wide, void* const* d,
+                    const void* g, int g_bits, int K, int r, int pre_entangled, void* const* d,
                     int d_bits, int64_t y_begin, int64_t n_out, int flavor,
-                    unsigned long long* mismatch_dev, void* stream) {
+                    unsigned long long* mismatch_dev, const void* imma_table, void* stream) {
   int st = check_conv_common(c_bits, g_bits, d_bits, K, n_in, period, y_begin, n_out);
   if (st) return st;
   if (add) NENT_CHECK_BITS(add_bits);
@@ -439,7 +440,7 @@ int nent_fused_conv(const void* const* c, int c_bits, int m, int64_t n_in, int64
   if (n_out == 0) return NENT_OK;
   ConvArgs A{};
   for (int i = 0; i < m; ++i) {
-    A.a.p[i] = c[(i + m - 1) % m];
+    A.a.p[i] = pre_entangled ? nullptr : c[(i + m - 1) % m];
     A.b.p[i] = c[i];
     A.y.p[i] = d[i];
   }
@@ -448,7 +449,7 @@ int nent_fused_conv(const void* const* c, int c_bits, int m, int64_t n_in, int64
   A.l = l; A.scale = scale; A.add = add; A.perm = perm;
   A.K = K; A.Kp = (K + CV_G - 1) / CV_G * CV_G;
   A.n_in = n_in; A.period = period; A.y_begin = y_begin; A.n_out = n_out;
-  A.g = g; A.r = r; A.wide = wide; A.mismatch = mismatch_dev;
+  A.g = g; A.r = r; A.wide = pre_entangled; A.mismatch = mismatch_dev; A.imma_table = imma_table;
   cudaStream_t s = as_stream(stream);
   if ((flavor & 0xff) == NENT_MAC_IMMA) return imma_dispatch(A, flavor, true, s);
   switch (flavor) {

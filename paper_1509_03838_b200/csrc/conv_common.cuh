@@ -20,6 +20,7 @@ struct ConvArgs {
   const int64_t* perm;
   const void* g;
   unsigned long long* mismatch;
+  const void* imma_table;  // prepared digit-split taps (nent_imma_table), or NULL
 };
 
 // x_row[p] after the on-load chain: entangle, scale, add, gather, zero-pad.

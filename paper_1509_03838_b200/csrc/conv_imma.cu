@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(IM_NT, 4)
       for (int s = 0; s < MS; ++s) {
         const int4 bv = raw4[(size_t)s * S4 + w];
         int64_t v[4] = {bv.x, bv.y, bv.z, bv.w};
-        if (EXTRACT) {  // eps_s = (c_{s-1} << l) + c_s, both tiles already in smem
+        if (EXTRACT && A.a.p[row0 + s]) {  // eps_s = (c_{s-1} << l) + c_s, both tiles in smem
           const int4 av = raw4[(size_t)((s + MS - 1) % MS) * S4 + w];
           v[0] = wadd(wshl(av.x, A.l), v[0]); v[1] = wadd(wshl(av.y, A.l), v[1]);
           v[2] = wadd(wshl(av.z, A.l), v[2]); v[3] = wadd(wshl(av.w, A.l), v[3]);
@@ -362,16 +362,28 @@ __global__ void __launch_bounds__(IM_NT, 4)
   }
 }
 
+// Keff/KD/segments for K taps and an output window starting at y_begin:
+// p0 = y_begin + tile*T - (Keff - 1) must be == 0 mod 4 (T is a multiple of 16)
+static void imma_geometry(int K, int64_t y_begin, ImmaGeom& Gm) {
+  Gm.Keff = K + (int)((((y_begin - K + 1) % 4) + 4) % 4);
+  Gm.KD = (Gm.Keff + 15 + 31) / 32 * 32;
+  Gm.NKC = Gm.KD / 32;
+  Gm.NSEG = (Gm.NKC + IM_SEG - 1) / IM_SEG;
+}
+static size_t imma_table_size(int nseg, int ng) { return (size_t)nseg * ng * 16 * IM_KDS; }
+static void launch_table(const void* g, int g_bits, int K, const ImmaGeom& Gm, int ng,
+                         unsigned char* table, cudaStream_t stream) {
+  const size_t tbytes = imma_table_size(Gm.NSEG, ng);
+  const unsigned blocks = (unsigned)((tbytes + 255) / 256 < 1024 ? (tbytes + 255) / 256 : 1024);
+  imma_table_kernel<<<blocks, 256, 0, stream>>>(g, g_bits, K, Gm.Keff, Gm.KD, ng, Gm.NSEG, table);
+}
+
 template <int MS, int NG, bool EXTRACT>
 static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
   constexpr int T = IM_T;
   ImmaGeom Gm{};
   Gm.np = np;
-  // p0 = y_begin + tile*T - (Keff - 1) must be == 0 mod 4 (T is a multiple of 16)
-  Gm.Keff = A.K + (int)((((A.y_begin - A.K + 1) % 4) + 4) % 4);
-  Gm.KD = (Gm.Keff + 15 + 31) / 32 * 32;
-  Gm.NKC = Gm.KD / 32;
-  Gm.NSEG = (Gm.NKC + IM_SEG - 1) / IM_SEG;
+  imma_geometry(A.K, A.y_begin, Gm);
   Gm.S = (T + Gm.NSEG * IM_SEG * 32 + 15) / 16 * 16;  // room for the last segment's k-steps
   Gm.bt_off = 0;
   Gm.pl_off = (NG * 16 * IM_KDS + 127) / 128 * 128;
@@ -392,22 +404,25 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
     }
     configured = Gm.smem;
   }
-  // digit-split Toeplitz taps, prepared once for the whole launch in a
-  // stream-ordered workspace (freed in stream order after the kernel)
-  const size_t tbytes = (size_t)Gm.NSEG * NG * 16 * IM_KDS;
+  // digit-split Toeplitz taps: the caller's prepared table, or one built for
+  // this launch in a stream-ordered workspace (freed in stream order after it)
   unsigned char* table = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&table), tbytes, stream) != cudaSuccess) {
-    set_error("imma conv: workspace allocation of %zu bytes failed", tbytes);
-    return NENT_ERR_CUDA;
+  if (A.imma_table) {
+    Gm.table = static_cast<const unsigned char*>(A.imma_table);
+  } else {
+    const size_t tbytes = imma_table_size(Gm.NSEG, NG);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&table), tbytes, stream) != cudaSuccess) {
+      set_error("imma conv: workspace allocation of %zu bytes failed", tbytes);
+      return NENT_ERR_CUDA;
+    }
+    launch_table(A.g, A.g_bits, A.K, Gm, NG, table, stream);
+    Gm.table = table;
   }
-  imma_table_kernel<<<(unsigned)((tbytes + 255) / 256 < 1024 ? (tbytes + 255) / 256 : 1024), 256, 0,
-                      stream>>>(A.g, A.g_bits, A.K, Gm.Keff, Gm.KD, NG, Gm.NSEG, table);
-  Gm.table = table;
   const int64_t tiles = (A.n_out + T - 1) / T;
   dim3 grid((unsigned)tiles, EXTRACT ? 1 : (unsigned)((A.rows + MS - 1) / MS));
   kern<<<grid, IM_NT, Gm.smem, stream>>>(A, Gm);
   const int st = check_launch("imma conv");
-  cudaFreeAsync(table, stream);
+  if (table) cudaFreeAsync(table, stream);
   return st;
 }
 
@@ -449,3 +464,32 @@ int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
 }
 
 }  // namespace nent
+
+using namespace nent;
+
+extern "C" {
+
+int64_t nent_imma_table_bytes(int K, int flavor) {
+  ImmaGeom Gm{};
+  imma_geometry(K, 0, Gm);
+  // K + 3 covers every y_begin residue (Keff <= K + 3)
+  ImmaGeom G3{};
+  imma_geometry(K + 3, 0, G3);
+  const int ng = (flavor >> 12) & 0xf;
+  return (int64_t)imma_table_size(G3.NSEG > Gm.NSEG ? G3.NSEG : Gm.NSEG, ng < 1 ? 1 : ng);
+}
+
+int nent_imma_table(const void* g, int g_bits, int K, int64_t y_begin, int flavor, void* table,
+                    void* stream) {
+  const int ng = (flavor >> 12) & 0xf;
+  if ((flavor & 0xff) != NENT_MAC_IMMA || ng < 1 || ng > 4 || K < 1 || (g_bits != 32 && g_bits != 64)) {
+    set_error("imma table: bad flavour 0x%x / K=%d", flavor, K);
+    return NENT_ERR_PARAM;
+  }
+  ImmaGeom Gm{};
+  imma_geometry(K, y_begin, Gm);
+  launch_table(g, g_bits, K, Gm, ng, static_cast<unsigned char*>(table), as_stream(stream));
+  return check_launch("imma table");
+}
+
+}  // extern "C"

@@ -38,6 +38,7 @@ class ChunkedEntangledConv:
         self.dev = device or D.device()
         self.g_dev = D.taps_tensor(self.g, flavor)
         m, H = params.m, self.K - 1
+        self.table = D.imma_table(self.g_dev, self.K, flavor, y_begin=H)  # every chunk starts at H
         self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(nstreams)]
         self.xbuf = [torch.empty((m, self.chunk + H), dtype=in_dtype, device=self.dev)
                      for _ in range(nstreams)]
@@ -80,7 +81,7 @@ class ChunkedEntangledConv:
                         xb[i, a - lo:b - lo].copy_(c_host[i, a:b], non_blocking=True)
                 D.fused_conv(xb[:, :width], self.g_dev, self.K, self.p.l, self.flavor, failed,
                              self.p.w > 32, period=width, n_in=width, y_begin=H, n_out=e - s,
-                             out=yb[:, : e - s])
+                             out=yb[:, : e - s], imma_table=self.table)
                 launches += 1
                 for i in range(m):
                     d_host[i, s:e].copy_(yb[i, : e - s], non_blocking=True)

@@ -21,7 +21,7 @@ P3 = nent.CodecParams(3, 32, 11, 10)
 def test_library_loaded_on_device():
     L = _lib.lib()
     assert L.nent_device_ok() == 1
-    assert L.nent_abi_version() == 1
+    assert L.nent_abi_version() == 2
 
 
 # ---- reference golden vectors (test_codec.py / test_ops.py) -----------------

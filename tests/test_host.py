@@ -147,7 +147,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
         assert s in _lib.SIGNATURES, f"{s} has no ctypes prototype"
-    assert L.nent_abi_version() == 1
+    assert L.nent_abi_version() == 2
 
 
 def test_library_is_sm100a():

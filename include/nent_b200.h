@@ -143,6 +143,17 @@ int nent_chain_conv(const void *a, const void *b, int in_bits, int64_t n_in, int
                     const void *g, int g_bits, int K, void *y, int y_bits, int64_t y_begin,
                     int64_t n_out, int flavor, const void *imma_table, void *stream);
 
+/* LSB chain in front of the conv (cfg5): entangle -> SCALE -> ADD (self-entangled
+ * kernel) -> PERMUTATION (ops.py:193-204, 219-220, 250-262), in two HBM passes:
+ * nent_interleave writes the m (<= 8) rows position-major (out[p*m + s] = x[s][p]),
+ * so each gathered position is one contiguous m-sample record; then
+ *   x[s][p] = scale * ((ct[q][s-1 mod m] << l) + ct[q][s]) + add[q],  q = perm ? perm[p] : p
+ * (add may be NULL).  Feed x to nent_fused_conv with pre_entangled = 1. */
+int nent_interleave(const void *const *x, int x_bits, int m, int64_t n, void *out, void *stream);
+int nent_gather_chain(const void *ct, int c_bits, int m, int64_t n, int l, int64_t scale,
+                      const void *add, int add_bits, const int64_t *perm, void *const *x, int x_bits,
+                      void *stream);
+
 /* ELEMENTWISE_ADD/SUB/MUL and SCALE (ops.py:193-204): y = x op g, g of length
  * n (g_len == n) or 1 (broadcast).  Arithmetic modulo 2^64; when check != 0
  * and op is MUL, *overflow_dev counts products that do not fit int64. */

@@ -255,6 +255,27 @@ def chain_conv(a: torch.Tensor | None, b: torch.Tensor, g_dev: torch.Tensor, K: 
     return out
 
 
+def interleave(x: torch.Tensor) -> torch.Tensor:
+    """(m, n) rows -> (n, m) position-major copy (m <= 8)."""
+    m, n = x.shape
+    out = torch.empty((n, m), dtype=x.dtype, device=x.device)
+    call("nent_interleave", row_ptrs(x), bits(x), m, n, ptr(out), _sh())
+    return out
+
+
+def gather_chain(ct: torch.Tensor, l: int, scale: int = 1, add: torch.Tensor | None = None,
+                 perm: torch.Tensor | None = None, out_dtype=torch.int32,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """Entangle -> scale -> add -> permute from the interleaved (n, m) streams;
+    returns the (m, n) chain output (entangled words, stream-major)."""
+    n, m = ct.shape
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype, device=ct.device)
+    call("nent_gather_chain", ptr(ct), bits(ct), m, n, l, int(scale), ptr(add),
+         bits(add) if add is not None else 64, ptr(perm), row_ptrs(out), bits(out), _sh())
+    return out
+
+
 def elementwise(x: torch.Tensor, g: torch.Tensor, op: int, check: bool, out_dtype=torch.int64):
     rows, n = x.shape
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)

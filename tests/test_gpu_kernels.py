@@ -262,3 +262,30 @@ def test_microbench_runs(kind):
     macs = D.microbench(kind, 148, 128, 10)
     torch.cuda.synchronize()
     assert macs == 148 * 128 * 10 * 16
+
+
+@pytest.mark.parametrize("m", [3, 5, 8])
+def test_interleave_gather_chain(oracle, m):
+    """entangle -> scale -> add (self-entangled) -> permute via interleave + gather."""
+    p = nent.derive_params(m, 32)
+    n = 5000
+    c = rand(m, (m, n), -100, 100)
+    add = rand(m + 1, (n,), -100, 100)
+    perm = np.random.default_rng(m).permutation(n).astype(np.int64)
+    scale = -7
+    eps = oracle.entangle(c, p.l)
+    ref = (eps * scale + oracle.self_entangle("add", add, p.l))[:, perm]
+    cd = torch.from_numpy(c).cuda().to(torch.int32)
+    ct = D.interleave(cd)
+    assert np.array_equal(ct.cpu().numpy(), c.T)
+    a = torch.from_numpy(add).cuda()
+    x = D.gather_chain(ct, p.l, scale, D.shift_add(a, a, p.l), torch.from_numpy(perm).cuda(),
+                       out_dtype=torch.int64)
+    assert np.array_equal(x.cpu().numpy(), ref)
+    # pre-entangled words through the fused conv + extract = the full chain conv
+    g = rand(m + 2, (40,), -50, 50)
+    want = oracle.full_conv((c * scale + add)[:, perm], g)
+    for fl in (MAC_I32, imma_flavor(D.signed_digits(int(np.abs(ref).max())), 1)):
+        d = D.fused_conv(x.to(torch.int32), D.taps_tensor(g, fl), 40, p.l, fl, 1, False, n + 39,
+                         n_in=n, pre_entangled=True)
+        assert np.array_equal(d.cpu().numpy(), want), fl

@@ -410,7 +410,18 @@ def check_shards(D, d_dev, rank, world, n, K, params, g, flavor, dev, xdev):
     for p in range(world):
         a, b = p * n, (p + 1) * n + (H if p == world - 1 else 0)
         want = sha(out[:, a:b].to(torch.int64).cpu().numpy())
-        ok = ok and want == bytes(hashes[p].cpu().numpy()).hex()
+        good = want == bytes(hashes[p].cpu().numpy()).hex()
+        if not good:
+            print(f"shard {p}: digest mismatch (mine {bytes(hashes[p].cpu().numpy()).hex()[:16]}, "
+                  f"want {want[:16]}; local {sha(d_dev.to(torch.int64).cpu().numpy())[:16] if p == 0 else ''})",
+                  file=sys.stderr)
+            if p == 0:
+                dd = d_dev.to(torch.int64).cpu().numpy()
+                ww = out[:, a:b].to(torch.int64).cpu().numpy()
+                bad = np.argwhere(dd != ww)
+                print(f"shard 0: {len(bad)} differing samples, first {bad[:4].tolist()}, "
+                      f"shapes {dd.shape} {ww.shape}", file=sys.stderr)
+        ok = ok and good
     return ok
 
 

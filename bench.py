@@ -137,7 +137,7 @@ def make_inputs(rank: int, n: int, K: int):
     slice from seed (2, p) -- same shapes and value distribution."""
     from paper_1509_03838_b200 import workloads
 
-    wl0 = workloads.make(2, n=n if rank == 0 else 16, K=K)
+    wl0 = workloads.make(2, n=n, K=K)  # the filter is drawn after the streams: full draw
     if rank == 0:
         return wl0.params, wl0.c, wl0.g
     rng = np.random.default_rng([2, rank])

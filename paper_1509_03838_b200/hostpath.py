@@ -108,3 +108,23 @@ class ChunkedEntangledConv:
     def synchronize(self):
         for st in (self.s_in, self.s_comp, self.s_out):
             st.synchronize()
+
+    def capture(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None):
+        """Record the whole job (every copy, kernel and cross-stream event) as
+        one CUDA graph on these host buffers; ``replay()`` then costs a single
+        launch instead of ~8 host calls per chunk."""
+        self.run(c_host, d_host, failed)  # warm: allocator, kernel attributes, tables
+        self.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=self.dev)
+        with torch.cuda.graph(self.graph, stream=cap):
+            for st in (self.s_in, self.s_comp, self.s_out):  # fork into the capture
+                st.wait_stream(cap)
+            self.run(c_host, d_host, failed)
+            for st in (self.s_in, self.s_comp, self.s_out):  # join back
+                cap.wait_stream(st)
+        torch.cuda.synchronize(self.dev)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()

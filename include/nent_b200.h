@@ -221,6 +221,22 @@ int nent_checksum_encode(const void *const *x, int x_bits, int m, int64_t n, voi
 int nent_checksum_recover(const void *const *x, int x_bits, const void *cs, int cs_bits, int m,
                           int64_t n, int failed, void *out, int out_bits, void *stream);
 
+/* ---- host <-> device staging ---------------------------------------------------- */
+
+#define NENT_COPY_H2D 1
+#define NENT_COPY_D2H 2
+#define NENT_COPY_D2D 3
+
+/* `rows` rows of `width_bytes` each, source rows `src_pitch` bytes apart,
+ * destination rows `dst_pitch` bytes apart, as ONE stream-ordered 2-D DMA
+ * (host side must be pinned for the copy to be asynchronous).  This is how a
+ * caller holding the reference's host StreamBlock (m rows of samples,
+ * blocks.py) stages a chunk of every stream at once: one copy-engine command
+ * per chunk and direction instead of one per row (the host-buffer pipeline's
+ * transfer primitive; paper_1509_03838_b200/hostpath.py). */
+int nent_copy_rows(void *dst, int64_t dst_pitch, const void *src, int64_t src_pitch,
+                   int64_t width_bytes, int rows, int direction, void *stream);
+
 /* ---- measurement ------------------------------------------------------------ */
 
 #define NENT_BENCH_IMMA 16 /* microbenchmark only: mma.sync m16n8k32 s8 (legacy IMMA) */

@@ -255,6 +255,27 @@ def chain_conv(a: torch.Tensor | None, b: torch.Tensor, g_dev: torch.Tensor, K: 
     return out
 
 
+def copy_rows(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst[:] = src for two (rows, width) views with contiguous rows and any
+    row pitch, one on the device and one in pinned host memory (or both on
+    the device), as one 2-D DMA on the current stream (nent_copy_rows)."""
+    if dst.shape != src.shape or dst.dim() != 2 or dst.dtype != src.dtype:
+        raise ParameterError("copy_rows needs two 2-D views of one shape and dtype")
+    if (dst.shape[1] > 1 and (dst.stride(1) != 1 or src.stride(1) != 1)):
+        raise ParameterError("copy_rows needs contiguous rows")
+    if dst.is_cuda and src.is_cuda:
+        direction = 3
+    elif dst.is_cuda:
+        direction = 1
+    elif src.is_cuda:
+        direction = 2
+    else:
+        raise ParameterError("copy_rows: one side must be on the device")
+    es = dst.element_size()
+    call("nent_copy_rows", dst.data_ptr(), dst.stride(0) * es, src.data_ptr(), src.stride(0) * es,
+         dst.shape[1] * es, dst.shape[0], direction, _sh())
+
+
 def interleave(x: torch.Tensor) -> torch.Tensor:
     """(m, n) rows -> (n, m) position-major copy (m <= 8)."""
     m, n = x.shape

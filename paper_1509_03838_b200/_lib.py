@@ -78,6 +78,7 @@ SIGNATURES = {
     "nent_check_range": [_PP, _I, _I, _L, _L, _P, _P],
     "nent_checksum_encode": [_PP, _I, _I, _L, _P, _I, _P],
     "nent_checksum_recover": [_PP, _I, _P, _I, _I, _L, _I, _P, _I, _P],
+    "nent_copy_rows": [_P, _L, _P, _L, _L, _I, _I, _P],
     "nent_microbench": [_I, _I, _I, _I, _P, ctypes.POINTER(ctypes.c_double), _P],
 }
 _RESTYPES = {"nent_last_error": ctypes.c_char_p, "nent_imma_table_bytes": ctypes.c_int64}

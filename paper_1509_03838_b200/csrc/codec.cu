@@ -385,4 +385,26 @@ int nent_checksum_recover(const void* const* x, int x_bits, const void* cs, int 
   return check_launch("checksum_recover");
 }
 
+int nent_copy_rows(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                   int64_t width_bytes, int rows, int direction, void* stream) {
+  static const cudaMemcpyKind kinds[4] = {cudaMemcpyDefault, cudaMemcpyHostToDevice,
+                                          cudaMemcpyDeviceToHost, cudaMemcpyDeviceToDevice};
+  if (direction < 1 || direction > 3 || rows < 0 || width_bytes < 0 ||
+      (rows > 1 && (dst_pitch < width_bytes || src_pitch < width_bytes))) {
+    set_error("copy_rows: bad direction %d / geometry (%lld x %d, pitches %lld, %lld)", direction,
+              (long long)width_bytes, rows, (long long)dst_pitch, (long long)src_pitch);
+    return NENT_ERR_PARAM;
+  }
+  if (rows == 0 || width_bytes == 0) return NENT_OK;
+  const size_t dp = rows > 1 ? (size_t)dst_pitch : (size_t)width_bytes;
+  const size_t sp = rows > 1 ? (size_t)src_pitch : (size_t)width_bytes;
+  cudaError_t e = cudaMemcpy2DAsync(dst, dp, src, sp, (size_t)width_bytes, (size_t)rows,
+                                    kinds[direction], as_stream(stream));
+  if (e != cudaSuccess) {
+    set_error("copy_rows: %s", cudaGetErrorString(e));
+    return NENT_ERR_CUDA;
+  }
+  return NENT_OK;
+}
+
 }  // extern "C"

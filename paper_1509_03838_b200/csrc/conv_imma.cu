@@ -159,11 +159,24 @@ __global__ void __launch_bounds__(IM_NT, 4)
   // ---- 1. stage: smem byte i of a plane <-> input position p0 + i ----
   const int64_t p0 = j0 - (Gm.Keff - 1);
   const uint64_t xbias = digit_bias(np);
-  bool fast = A.in_bits == 32 && !A.perm && A.scale == 1 && !A.add && p0 >= 0 && p0 + S <= A.n_in;
+  // Raw rows arrive by TMA from the 16-byte-aligned word at or below p0, so a
+  // row base that is only 4-byte aligned (a sliced or halo-prefixed buffer)
+  // still takes the bulk-copy path; mis[s] words of lead-in are skipped.
+  const int RS = S + 4;
+  int mis[MS];
+  bool fast = A.in_bits == 32 && !A.perm && A.scale == 1 && !A.add;
 #pragma unroll
   for (int s = 0; s < MS; ++s) {
     const int row = row0 + s;
-    fast = fast && row < A.rows && ((uintptr_t)A.b.p[row] & 15) == 0 && (EXTRACT || !A.a.p[row]);
+    mis[s] = 0;
+    if (row < A.rows) {
+      const uintptr_t q = reinterpret_cast<uintptr_t>(reinterpret_cast<const int32_t*>(A.b.p[row]) + p0);
+      mis[s] = (int)((q & 15) >> 2);
+      fast = fast && (q & 3) == 0 && p0 - mis[s] >= 0 && p0 - mis[s] + S + (mis[s] ? 4 : 0) <= A.n_in;
+    } else {
+      fast = false;
+    }
+    fast = fast && (EXTRACT || !A.a.p[row]);
   }
   if (tid == 0) {
     mbar_init(mb_raw);
@@ -177,21 +190,29 @@ __global__ void __launch_bounds__(IM_NT, 4)
   if (fast) {
     int32_t* raw = reinterpret_cast<int32_t*>(dt);
     if (tid == 0) {
-      mbar_expect(mb_raw, (uint32_t)(MS * S * 4));
+      uint32_t total = 0;
+#pragma unroll
+      for (int s = 0; s < MS; ++s) total += (uint32_t)(S + (mis[s] ? 4 : 0)) * 4u;
+      mbar_expect(mb_raw, total);
 #pragma unroll
       for (int s = 0; s < MS; ++s)
-        bulk_g2s((uint32_t)__cvta_generic_to_shared(raw + (size_t)s * S),
-                 reinterpret_cast<const int32_t*>(A.b.p[row0 + s]) + p0, (uint32_t)(S * 4), mb_raw);
+        bulk_g2s((uint32_t)__cvta_generic_to_shared(raw + (size_t)s * RS),
+                 reinterpret_cast<const int32_t*>(A.b.p[row0 + s]) + p0 - mis[s],
+                 (uint32_t)(S + (mis[s] ? 4 : 0)) * 4u, mb_raw);
     }
     mbar_wait(mb_raw, 0);
-    const int4* raw4 = reinterpret_cast<const int4*>(raw);
+    auto word4 = [&](int s, int w) -> int4 {
+      if (mis[s] == 0) return reinterpret_cast<const int4*>(raw + (size_t)s * RS)[w];
+      const int32_t* r = raw + (size_t)s * RS + mis[s] + 4 * w;
+      return make_int4(r[0], r[1], r[2], r[3]);
+    };
     for (int w = tid; w < S4; w += IM_NT) {
 #pragma unroll
       for (int s = 0; s < MS; ++s) {
-        const int4 bv = raw4[(size_t)s * S4 + w];
+        const int4 bv = word4(s, w);
         int64_t v[4] = {bv.x, bv.y, bv.z, bv.w};
         if (EXTRACT && A.a.p[row0 + s]) {  // eps_s = (c_{s-1} << l) + c_s, both tiles in smem
-          const int4 av = raw4[(size_t)((s + MS - 1) % MS) * S4 + w];
+          const int4 av = word4((s + MS - 1) % MS, w);
           v[0] = wadd(wshl(av.x, A.l), v[0]); v[1] = wadd(wshl(av.y, A.l), v[1]);
           v[2] = wadd(wshl(av.z, A.l), v[2]); v[3] = wadd(wshl(av.w, A.l), v[3]);
         }
@@ -388,7 +409,7 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
   Gm.bt_off = 0;
   Gm.pl_off = (NG * 16 * IM_KDS + 127) / 128 * 128;
   Gm.dt_off = (Gm.pl_off + MS * np * Gm.S + 127) / 128 * 128;
-  const size_t dt_bytes = (size_t)MS * T * 8, raw_bytes = (size_t)MS * Gm.S * 4;
+  const size_t dt_bytes = (size_t)MS * T * 8, raw_bytes = (size_t)MS * (Gm.S + 4) * 4;
   Gm.smem = (size_t)Gm.dt_off + (dt_bytes > raw_bytes ? dt_bytes : raw_bytes);
   if (Gm.smem > 227 * 1024) {
     set_error("imma conv: tile needs %zu bytes of shared memory (K=%d too long)", Gm.smem, A.K);

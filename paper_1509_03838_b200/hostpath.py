@@ -20,38 +20,82 @@ from .errors import ParameterError
 from .params import CodecParams
 
 
+PRE = 64    # device lead-in words before each input window (host reads start 256-byte aligned)
+LEAD = 64   # extra outputs computed before each chunk (host writes start 256-byte aligned)
+ALIGN = 256  # pinned DMA runs at full duplex rate only from/to 256-byte-aligned host addresses
+
+
 class ChunkedEntangledConv:
     """Reusable pipeline for one geometry: m streams of n samples, K taps.
 
     Inputs/outputs are pinned host tensors (int32 or int64); outputs are the
-    recovered full-convolution samples, n + K - 1 per stream."""
+    recovered full-convolution samples, n + K - 1 per stream.
 
-    def __init__(self, params: CodecParams, n: int, g, flavor: int, chunk: int = 1 << 21,
+    Each chunk moves as ONE 2-D DMA per direction (all m rows, nent_copy_rows)
+    -- per-row copies cost ~5% at 2^20-sample chunks and ~20% at 2^18.  Host
+    transfers start on a 256-byte boundary (row 0's; other rows follow the
+    caller's pitch): concurrent H2D + D2H loses ~20% when the host side is
+    misaligned (scripts/pcie_align_probe.py), so each input copy starts at the
+    aligned word at or below its window (the kernel reads its rows from
+    ``PRE`` words in), and each chunk computes ``LEAD`` extra outputs before
+    its window so its output copy can start at the aligned word at or below
+    the chunk boundary.  ``ramp`` > 0 shrinks the first and last chunks
+    (chunk / 2^ramp ...); with the output lag below it does not pay on cfg2.
+
+    Output copies lag the input copies by ``lag`` chunks (chunk j's D2H also
+    waits for chunk j + lag's H2D).  Without it the two directions run in
+    lockstep -- H2D(j+1) and D2H(j) share the link and finish together -- and
+    every chunk's kernel then sits exposed on the D2H stream: an idle output
+    direction does not make the input direction much faster, so the input
+    side never builds the lead that would hide it (scripts/e2e_isolate.py)."""
+
+    def __init__(self, params: CodecParams, n: int, g, flavor: int, chunk: int = 1 << 20,
                  in_dtype=torch.int32, out_dtype=torch.int32, nbuf: int = 4,
-                 device: torch.device | None = None):
+                 device: torch.device | None = None, ramp: int = 0, lag: int = 1):
         self.p = params
         self.n = n
         self.g = np.asarray(g, dtype=np.int64)
         self.K = len(self.g)
         self.L = n + self.K - 1
         self.flavor = flavor
-        self.chunk = min(chunk, self.L)
+        self.bounds = self._schedule(self.L, max(chunk, 1024), ramp)
+        self.chunk = max(e - s for s, e in self.bounds)
         self.in_dtype, self.out_dtype = in_dtype, out_dtype
         self.dev = device or D.device()
         self.g_dev = D.taps_tensor(self.g, flavor)
         m, H = params.m, self.K - 1
-        self.table = D.imma_table(self.g_dev, self.K, flavor, y_begin=H)  # every chunk starts at H
+        self.table = D.imma_table(self.g_dev, self.K, flavor, y_begin=H)  # every chunk's window starts at H
         self.s_in = torch.cuda.Stream(device=self.dev)
         self.s_comp = torch.cuda.Stream(device=self.dev)
         self.s_out = torch.cuda.Stream(device=self.dev)
-        self.nbuf = nbuf
-        self.xbuf = [torch.empty((m, self.chunk + H), dtype=in_dtype, device=self.dev) for _ in range(nbuf)]
-        self.ybuf = [torch.empty((m, self.chunk), dtype=out_dtype, device=self.dev) for _ in range(nbuf)]
+        if not 0 <= lag < nbuf:
+            raise ParameterError(f"lag {lag} must be in [0, nbuf)")
+        self.nbuf, self.lag = nbuf, lag
+        row = (PRE + LEAD + self.chunk + H + 31) // 32 * 32  # 128-byte row starts
+        self.xbuf = [torch.empty((m, row), dtype=in_dtype, device=self.dev) for _ in range(nbuf)]
+        self.ybuf = [torch.empty((m, LEAD + self.chunk), dtype=out_dtype, device=self.dev)
+                     for _ in range(nbuf)]
         self.launches = 0
 
+    @staticmethod
+    def _schedule(L: int, chunk: int, ramp: int) -> list[tuple[int, int]]:
+        head = [chunk >> k for k in range(ramp, 0, -1) if chunk >> k >= 4096]
+        if 2 * sum(head) + chunk > L:
+            head = []
+        mid = L - 2 * sum(head)
+        nmid = max(1, -(-mid // chunk))
+        step = ((mid + nmid - 1) // nmid + 63) // 64 * 64 if nmid > 1 else mid
+        sizes = head + [step] * (nmid - 1) + [mid - step * (nmid - 1)] + head[::-1]
+        out, s = [], 0
+        for z in sizes:
+            if z > 0:
+                out.append((s, s + z))
+                s += z
+        assert s == L
+        return out
+
     def chunks(self):
-        for s in range(0, self.L, self.chunk):
-            yield s, min(s + self.chunk, self.L)
+        yield from self.bounds
 
     def h2d_bytes(self) -> int:
         es = torch.tensor([], dtype=self.in_dtype).element_size()
@@ -61,47 +105,84 @@ class ChunkedEntangledConv:
         es = torch.tensor([], dtype=self.out_dtype).element_size()
         return self.p.m * self.L * es
 
+    @staticmethod
+    def _lead(t: torch.Tensor, i: int, j: int) -> int:
+        """Words between t[i, j] and the 256-byte boundary at or below it."""
+        addr = t.data_ptr() + (i * t.stride(0) + j * t.stride(1)) * t.element_size()
+        return (addr % ALIGN) // t.element_size()
+
+    def _h2d(self, xb, c_host, lo, a, b):
+        """Input window [a, b) of every row -> xb (device word PRE + p - lo
+        holds sample p), one 2-D DMA starting at row 0's aligned word."""
+        a0 = max(a - self._lead(c_host, 0, a), 0)
+        D.copy_rows(xb[:, PRE + a0 - lo:PRE + b - lo], c_host[:, a0:b])
+
+    def _d2h(self, d_host, yb, h0, h1, ys):
+        """Outputs [h0, h1) of every row -> host (yb word q holds ys + q)."""
+        if h1 > h0:
+            D.copy_rows(d_host[:, h0:h1], yb[:, h0 - ys:h1 - ys])
+
     def run(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None) -> int:
         """Enqueue the whole job; returns the number of kernels launched.
         Call ``synchronize()`` before reading ``d_host``."""
         if not c_host.is_pinned() or not d_host.is_pinned():
             raise ParameterError("host buffers must be pinned (torch.empty(..., pin_memory=True))")
-        m, H, n = self.p.m, self.K - 1, self.n
-        in_done = [torch.cuda.Event() for _ in range(self.nbuf)]
-        comp_done = [None] * self.nbuf
-        out_done = [None] * self.nbuf
+        m, H, n, L = self.p.m, self.K - 1, self.n, self.L
+        if tuple(c_host.shape) != (m, n) or tuple(d_host.shape) != (m, L):
+            raise ParameterError(f"expected c_host {(m, n)} and d_host {(m, L)}")
+        if c_host.stride(1) != 1 or d_host.stride(1) != 1:
+            raise ParameterError("host rows must be contiguous")
+        nch = len(self.bounds)
+        in_ev = [torch.cuda.Event() for _ in range(nch)]
+        comp_ev = [torch.cuda.Event() for _ in range(nch)]
+        out_ev = [torch.cuda.Event() for _ in range(nch)]
+        # output copy starts: row 0's aligned word at or below each chunk boundary
+        hs = [0] + [max(s - self._lead(d_host, 0, s), 0) for s, _ in self.bounds[1:]] + [L]
+
+        def d2h(j):
+            """Copy chunk j's outputs back once its kernel is done and, with
+            lag, once the input of chunk j + lag has arrived."""
+            s, e = self.bounds[j]
+            ys = max(s - LEAD, 0)
+            yb = self.ybuf[j % self.nbuf]
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(comp_ev[j])
+                if j + self.lag < nch:
+                    self.s_out.wait_event(in_ev[j + self.lag])
+                self._d2h(d_host, yb, hs[j], hs[j + 1], ys)
+                out_ev[j].record(self.s_out)
+
         launches = 0
-        for idx, (s, e) in enumerate(self.chunks()):
+        for idx, (s, e) in enumerate(self.bounds):
             k = idx % self.nbuf
             xb, yb = self.xbuf[k], self.ybuf[k]
-            lo, hi = s - H, e  # input window [lo, hi) of this chunk
+            ys = max(s - LEAD, 0)  # this chunk's outputs [ys, e)
+            lo, hi = ys - H, e     # and its input window [lo, hi)
             a, b = max(lo, 0), min(hi, n)
             width = hi - lo
             with torch.cuda.stream(self.s_in):
-                if comp_done[k] is not None:  # the kernel that last read xb has finished
-                    self.s_in.wait_event(comp_done[k])
-                if lo < 0 or hi > n:
-                    xb[:, :width].zero_()
+                if idx >= self.nbuf:  # the kernel that last read xb has finished
+                    self.s_in.wait_event(comp_ev[idx - self.nbuf])
+                if lo < 0:
+                    xb[:, PRE:PRE - lo].zero_()
+                if hi > n:
+                    xb[:, PRE + max(n - lo, 0):PRE + width].zero_()
                 if b > a:
-                    for i in range(m):
-                        xb[i, a - lo:b - lo].copy_(c_host[i, a:b], non_blocking=True)
-                in_done[k].record(self.s_in)
+                    self._h2d(xb, c_host, lo, a, b)
+                in_ev[idx].record(self.s_in)
             with torch.cuda.stream(self.s_comp):
-                self.s_comp.wait_event(in_done[k])
-                if out_done[k] is not None:  # the copy that last read yb has finished
-                    self.s_comp.wait_event(out_done[k])
-                D.fused_conv(xb[:, :width], self.g_dev, self.K, self.p.l, self.flavor, failed,
-                             self.p.w > 32, period=width, n_in=width, y_begin=H, n_out=e - s,
-                             out=yb[:, : e - s], imma_table=self.table)
+                self.s_comp.wait_event(in_ev[idx])
+                if idx >= self.nbuf:  # the copy that last read yb has finished
+                    self.s_comp.wait_event(out_ev[idx - self.nbuf])
+                D.fused_conv(xb[:, PRE:PRE + width], self.g_dev, self.K, self.p.l, self.flavor, failed,
+                             self.p.w > 32, period=width, n_in=width, y_begin=H, n_out=e - ys,
+                             out=yb[:, : e - ys], imma_table=self.table)
                 launches += 1
-                comp_done[k] = torch.cuda.Event()
-                comp_done[k].record(self.s_comp)
-            with torch.cuda.stream(self.s_out):
-                self.s_out.wait_event(comp_done[k])
-                for i in range(m):
-                    d_host[i, s:e].copy_(yb[i, : e - s], non_blocking=True)
-                out_done[k] = torch.cuda.Event()
-                out_done[k].record(self.s_out)
+                comp_ev[idx].record(self.s_comp)
+            if idx - self.lag >= 0:
+                d2h(idx - self.lag)
+        for j in range(max(nch - self.lag, 0), nch):
+            d2h(j)
         self.launches = launches
         return launches
 

@@ -131,6 +131,30 @@ def test_conv_halo_windows(oracle):
             assert np.array_equal(y.cpu().numpy(), ref[:, y0:y0 + cnt]), (flavor, y0, cnt)
 
 
+@pytest.mark.parametrize("off,pad", [(0, 0), (1, 0), (2, 5), (3, 1), (1, 3)])
+def test_imma_unaligned_rows(oracle, off, pad):
+    """Row bases that are only 4-byte aligned (sliced buffers, halo-prefixed
+    shards: row stride n + K - 1) take the bulk-copy staging from the aligned
+    word below; every lead-in offset and both kernel modes stay exact."""
+    n, K = 9000 + pad, 256
+    p = nent.derive_params(3, 64)  # the cfg2 codec: l = 21 admits these outputs
+    c = rand(off * 10 + pad, (3, n), -2048, 2047)
+    g = rand(off + pad, (K,), -2048, 2047)
+    ref = oracle.full_conv(c, g)
+    big = torch.zeros((3, n + off + pad), dtype=torch.int32, device="cuda")
+    big[:, off:off + n] = torch.from_numpy(c).to(torch.int32)
+    x = big[:, off:off + n]
+    eb = 2048 * ((1 << p.l) + 1)
+    fl = fused.conv_flavor(eb, g, n_out=1 << 30)
+    assert is_imma(fl)
+    for r in (None, 0, 2):
+        res = fused.entangled_conv(nent.StreamBlock(p, x), g, failed=r, flavor=fl)
+        assert np.array_equal(res.outputs.data.cpu().numpy(), ref), (off, pad, r)
+    fl_plain = imma_flavor(D.signed_digits(2048), D.signed_digits(2048))
+    y, _ = D.conv(x, D.taps_tensor(g, fl_plain), K, fl_plain, period=n + K - 1)
+    assert np.array_equal(y.cpu().numpy(), ref), (off, pad)
+
+
 @pytest.mark.parametrize("m,w", [(3, 32), (4, 32), (5, 32), (8, 32), (3, 64), (4, 64), (3, 48),
                                  (6, 64), (7, 64)])
 def test_fused_conv_every_failure(oracle, m, w):

@@ -45,11 +45,16 @@ extern "C" {
 #define NENT_MAC_G64 5 /* generic 64x64 low product (mul.lo.u64)                        */
 #define NENT_MAC_X128 6 /* exact 128-bit accumulation + overflow count (object path)    */
 /* Tensor-core digit slicing: x and g split into balanced base-256 int8 digits
- * (np planes of x, ng digits of g), every digit pair convolved with
- * mma.sync m16n8k32 s8 (int32 exact), recombined mod 2^64.  Exact whenever the
- * result fits int64, np <= 8, ng <= 4, K + 15 < 65536. */
+ * (np planes of x, ng digits of g), every digit pair an exact int8 GEMM with
+ * int32 accumulation, recombined mod 2^64.  Exact whenever the result fits
+ * int64, np <= 8, ng <= 4, K + 15 < 65536.  Runs on the 5th-generation tensor
+ * cores (tcgen05.mma kind::i8, TMEM accumulators) when the shape fits that
+ * kernel (plain conv of <= 64 rows, or the fused m = 3 path; K + 127 taps of
+ * every digit resident in shared memory), else on mma.sync m16n8k32 s8.
+ * NENT_IMMA_MMA_SYNC forces the mma.sync kernel. */
 #define NENT_MAC_IMMA 7
 #define NENT_MAC_IMMA_DIGITS(np, ng) (NENT_MAC_IMMA | ((np) << 8) | ((ng) << 12))
+#define NENT_IMMA_MMA_SYNC (1 << 16)
 
 /* Elementwise op codes (ops.py:193-204). */
 #define NENT_EW_ADD 0

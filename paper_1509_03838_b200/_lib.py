@@ -21,10 +21,14 @@ MAC_I32, MAC_F64, MAC_W64, MAC_S64, MAC_G64, MAC_X128, MAC_IMMA = 1, 2, 3, 4, 5,
 BENCH_IMMA = 16
 
 
-def imma_flavor(np_: int, ng: int) -> int:
+IMMA_MMA_SYNC = 1 << 16  # NENT_IMMA_MMA_SYNC: force the mma.sync kernel
+
+
+def imma_flavor(np_: int, ng: int, mma_sync: bool = False) -> int:
     """NENT_MAC_IMMA_DIGITS(np, ng): tensor-core digit slicing with np planes of x
-    and ng digits of g (balanced base-256)."""
-    return MAC_IMMA | (np_ << 8) | (ng << 12)
+    and ng digits of g (balanced base-256); tcgen05 where the shape fits it,
+    mma.sync otherwise or when ``mma_sync``."""
+    return MAC_IMMA | (np_ << 8) | (ng << 12) | (IMMA_MMA_SYNC if mma_sync else 0)
 
 
 def is_imma(flavor: int) -> bool:
@@ -34,7 +38,7 @@ def is_imma(flavor: int) -> bool:
 class _FlavorNames(dict):
     def __missing__(self, key):
         if is_imma(key):
-            return f"imma{(key >> 8) & 15}x{(key >> 12) & 15}"
+            return f"imma{(key >> 8) & 15}x{(key >> 12) & 15}" + ("-mma.sync" if key & IMMA_MMA_SYNC else "")
         raise KeyError(key)
 
 

@@ -95,7 +95,10 @@ __device__ __forceinline__ void stage_row(const ConvArgs& A, int row, int64_t p0
 }
 
 
-// tensor-core digit-sliced convolution (conv_imma.cu)
+// tensor-core digit-sliced convolution: tcgen05 (conv_tc05.cu) where the shape
+// fits its envelope, else mma.sync (conv_imma.cu)
 int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s);
+constexpr int NENT_TC05_NA = 1000;  // tc05_conv: shape outside the tcgen05 kernel's envelope
+int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s);
 
 }  // namespace nent

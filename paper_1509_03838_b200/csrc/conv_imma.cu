@@ -476,6 +476,10 @@ int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
     set_error("imma conv: digit counts np=%d ng=%d outside 1..8 / 1..4", np, ng);
     return NENT_ERR_PARAM;
   }
+  if (!(flavor & NENT_IMMA_MMA_SYNC)) {
+    const int st = tc05_conv(A, np, ng, extract, s);
+    if (st != NENT_TC05_NA) return st;
+  }
   switch (ng) {
     case 1: return imma_dispatch_ng<1>(A, np, extract, s);
     case 2: return imma_dispatch_ng<2>(A, np, extract, s);

@@ -1,0 +1,126 @@
+// tc05.cuh -- thin sm_100a wrappers for the 5th-generation tensor-core path:
+// TMEM allocation, tcgen05.mma (kind::i8, A from TMEM or shared memory),
+// commit-to-mbarrier, TMEM loads/stores, and the shared-memory matrix /
+// instruction descriptors.  Bit layouts follow the PTX ISA descriptors for
+// sm_100 (smem descriptor version 1, SWIZZLE_128B = layout type 2).
+#pragma once
+
+#include <cstdint>
+
+namespace nent {
+namespace tc05 {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// ---- TMEM allocation (one full warp) -------------------------------------
+__device__ __forceinline__ void alloc(uint32_t* smem_slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_slot)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+// ---- ordering ----------------------------------------------------------------
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---- TMEM <-> registers: warp w reaches lanes [32(w%4), 32(w%4)+32) ----------
+__device__ __forceinline__ void st_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(r[0]),
+      "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+__device__ __forceinline__ void ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+// ---- descriptors --------------------------------------------------------------
+// Instruction descriptor: 8-bit integer A (signed) x B (signed or unsigned)
+// -> s32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool b_signed = true) {
+  return (2u << 4)                    // D format s32
+         | (1u << 7)                  // A signed 8-bit
+         | ((b_signed ? 1u : 0u) << 10)
+         | ((uint32_t)(N >> 3) << 17)  // N / 8
+         | ((uint32_t)(M >> 4) << 24); // M / 16
+}
+// K-major SWIZZLE_128B shared-memory matrix: rows 128 B apart, 8-row groups
+// 1024 B apart (SBO); the 16-byte chunks of each row are XOR-swizzled by
+// address bits [7,10), so a start address advanced by any multiple of 16 B
+// (a K step inside the row, or whole rows) stays consistent with data written
+// through sw128().
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// physical byte offset of logical offset L inside a 1024-B-aligned SW128 region
+__host__ __device__ __forceinline__ uint32_t sw128(uint32_t L) { return L ^ (((L >> 7) & 7u) << 4); }
+
+// ---- MMA ---------------------------------------------------------------------------
+// D[tmem] (+)= A[tmem] . B[smem]^T   (A: M x 32 int8 in 8 TMEM columns per lane)
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// D[tmem] (+)= A[smem] . B[smem]^T
+__device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// Warp-collective forms: the whole (converged) warp executes them with
+// warp-uniform operands and one elected lane issues, so descriptors stay in
+// uniform registers instead of a per-MMA waterfall loop.
+__device__ __forceinline__ void mma_i8_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_elect(uint32_t mbar_saddr) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(mbar_saddr)
+      : "memory");
+}
+
+// SW128 descriptor high word (SBO = 1024 B, version 1, layout SWIZZLE_128B):
+// constant, so only the low word (start address >> 4 | LBO << 16) varies.
+constexpr uint32_t SW128_DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
+__host__ __device__ constexpr uint32_t desc_sw128_lo(uint32_t saddr) { return ((saddr & 0x3FFFF) >> 4) | (1u << 16); }
+// D[tmem] (+)= A[tmem] . B[smem]^T with B given by its descriptor low word
+__device__ __forceinline__ void mma_i8_ts_lo(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 bd;\n setp.ne.b32 p, %4, 0;\n mov.b64 bd, {%2, %5};\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], bd, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(SW128_DESC_HI));
+}
+
+// arrive once on an mbarrier when every MMA issued so far by this thread is done
+__device__ __forceinline__ void commit(uint32_t mbar_saddr) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar_saddr)
+               : "memory");
+}
+
+}  // namespace tc05
+}  // namespace nent

@@ -131,6 +131,31 @@ def test_conv_halo_windows(oracle):
             assert np.array_equal(y.cpu().numpy(), ref[:, y0:y0 + cnt]), (flavor, y0, cnt)
 
 
+@pytest.mark.parametrize("K", [1, 64, 129, 200, 257, 300])
+@pytest.mark.parametrize("bits", [7, 12, 20])
+def test_tcgen05_and_mma_sync_kernels(oracle, K, bits):
+    """Both tensor-core kernels (tcgen05 where the shape fits it: K <= 257,
+    np <= 6; mma.sync otherwise or when forced) agree with the oracle, plain
+    and fused, for every failure index, on tile-edge lengths."""
+    n = 3 * 8192 + 77  # several 8192-output tiles plus a ragged one
+    lim = 1 << bits
+    p = nent.derive_params(3, 64)
+    c = rand(K + bits, (3, n), -lim, lim - 1)
+    g = rand(K * 3 + bits, (K,), -lim, lim - 1)
+    ref = oracle.full_conv(c, g)
+    xd = torch.from_numpy(c).cuda().to(torch.int32)
+    for mma_sync in (False, True):
+        fl = imma_flavor(D.signed_digits(lim), D.signed_digits(lim), mma_sync)
+        y, _ = D.conv(xd, D.taps_tensor(g, fl), K, fl, period=n + K - 1)
+        assert np.array_equal(y.cpu().numpy(), ref), ("plain", K, bits, mma_sync)
+        fl = imma_flavor(D.signed_digits(lim * ((1 << p.l) + 1)), D.signed_digits(lim), mma_sync)
+        for r in (None, 0, 1, 2):
+            res = fused.entangled_conv(nent.StreamBlock(p, xd), g, failed=r, flavor=fl)
+            assert np.array_equal(res.outputs.data.cpu().numpy(), ref), ("fused", K, bits, mma_sync, r)
+            if r is None:
+                assert res.mismatches == 0
+
+
 @pytest.mark.parametrize("off,pad", [(0, 0), (1, 0), (2, 5), (3, 1), (1, 3)])
 def test_imma_unaligned_rows(oracle, off, pad):
     """Row bases that are only 4-byte aligned (sliced buffers, halo-prefixed

@@ -7,8 +7,9 @@ geometry derive_params(3, 64) = (l=21, k=21); full linear convolution of every
 entangled stream, all 3 outputs recovered (failed=None pivots on stream 0 and
 checks the redundant stream).  One step = one launch of the fused
 entangle -> conv -> extract kernel over the whole batch, inputs resident in HBM.
-The kernel is the exact digit-sliced tensor-core convolution (IMMA, mma.sync
-s8): the 35-bit entangled words become 5 int8 digit planes, the 12-bit taps 2.
+The kernel is the exact digit-sliced tensor-core convolution on the 5th-gen
+tensor cores (tcgen05.mma kind::i8, TMEM accumulators, warp-specialised): the
+35-bit entangled words become 5 int8 digit planes, the 12-bit taps 2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -163,7 +164,7 @@ def run_ours(args):
 
     from paper_1509_03838_b200 import _device as D
     from paper_1509_03838_b200 import fused
-    from paper_1509_03838_b200._lib import (BENCH_IMMA, MAC_F64, MAC_G64, MAC_I32, MAC_NAMES, MAC_S64,
+    from paper_1509_03838_b200._lib import (BENCH_IMMA, BENCH_TC05, MAC_F64, MAC_G64, MAC_I32, MAC_NAMES, MAC_S64,
                                             MAC_W64, imma_flavor, is_imma)
     from paper_1509_03838_b200.hostpath import ChunkedEntangledConv
 
@@ -279,13 +280,15 @@ def run_ours(args):
 
     # ---------------- measured pipe peaks (roofline denominators) ----------------
     peaks = {}
-    for kind in (BENCH_IMMA, MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64):
-        D.microbench(kind, 148 * 4, 256, 64)
+    for kind in (BENCH_TC05, BENCH_IMMA, MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64):
+        grid = 148 if kind == BENCH_TC05 else 148 * 8
+        iters = {BENCH_TC05: 2000, BENCH_IMMA: 1024}.get(kind, 4096)
+        D.microbench(kind, grid, 256, 64)
         best = 0.0
         for _ in range(3):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            macs = D.microbench(kind, 148 * 8, 256, 4096 if kind != BENCH_IMMA else 1024)
+            macs = D.microbench(kind, grid, 256, iters)
             b.record(stream)
             torch.cuda.synchronize(dev)
             best = max(best, macs / (a.elapsed_time(b) / 1e3))
@@ -295,7 +298,11 @@ def run_ours(args):
     macs_alg = m * n * K                      # M*N*K
     digit_macs = macs_alg * np_ * ng          # int8 digit products the method needs
     achieved = 2 * digit_macs / (kern_ms / 1e3) / 1e12
-    peak = 2 * peaks["imma_s8_mma_sync"] / 1e12
+    kernel_kind = D.imma_kernel(flavor, K, m, True)
+    peak_key = "tcgen05_i8" if kernel_kind == "tcgen05" else "imma_s8_mma_sync"
+    peak = 2 * peaks[peak_key] / 1e12
+    kt = (K + 127 + 127) // 128 * 128      # tcgen05 Toeplitz band: K + 127 padded to 128
+    issued_macs = m * (n + K - 1) * kt * np_ * ng if kernel_kind == "tcgen05" else None
     traffic = None
     tf = REPO / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -365,14 +372,24 @@ def run_ours(args):
                 "note": "plain_same_kernel runs the identical kernel/digit geometry on the plain streams "
                         "(isolates entangle+extract); plain_fastest uses the digits the 12-bit plain "
                         "samples need (2 planes instead of the entangled words' 5)"},
-            "roofline": {"bound": "tensor", "pipe": "IMMA (mma.sync m16n8k32 s8, tensor cores)",
+            "roofline": {"bound": "tensor",
+                         "pipe": ("tcgen05.mma kind::i8 (5th-gen tensor cores, TMEM accumulators)"
+                                  if kernel_kind == "tcgen05" else "IMMA (mma.sync m16n8k32 s8)"),
                          "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": f"nent::conv_imma_kernel<3,{ng},true> ({MAC_NAMES[flavor]})",
+                         "kernel": (f"nent::tcc::conv_tc05_kernel<true,{np_},{kt // 32}> ({MAC_NAMES[flavor]})"
+                                    if kernel_kind == "tcgen05"
+                                    else f"nent::conv_imma_kernel<3,{ng},true> ({MAC_NAMES[flavor]})"),
                          "algorithmic_per_launch": {"conv_macs": macs_alg, "digit_macs": digit_macs,
-                                                    "digit_planes": np_, "tap_digits": ng},
-                         "peak_source": "measured in this run: nent_microbench mma.sync s8 "
-                                        "(16 independent accumulators per warp, 148*8 CTAs x 8 warps)",
+                                                    "digit_planes": np_, "tap_digits": ng,
+                                                    "tensor_macs_issued": issued_macs,
+                                                    "note": "achieved counts the method's digit MACs "
+                                                            "(M*N*K*np*ng); the tcgen05 Toeplitz band "
+                                                            "issues KT/K more (zero taps outside the band)"},
+                         "issued_tops": (2 * issued_macs / (kern_ms / 1e3) / 1e12) if issued_macs else None,
+                         "peak_source": (f"measured in this run: nent_microbench {peak_key} "
+                                         + ("(tcgen05.mma 128x128x32 chains, 1 CTA/SM)" if kernel_kind == "tcgen05"
+                                            else "(16 independent accumulators per warp, 148*8 CTAs x 8 warps)")),
                          "cuda_core_path": {"flavor": MAC_NAMES[core_flavor],
                                             "achieved_tflops": 2 * macs_alg / (med["entangled_cuda_core"] / 1e3) / 1e12,
                                             "peak_tflops": 2 * peaks[MAC_NAMES[core_flavor]] / 1e12},

@@ -56,6 +56,11 @@ extern "C" {
 #define NENT_MAC_IMMA_DIGITS(np, ng) (NENT_MAC_IMMA | ((np) << 8) | ((ng) << 12))
 #define NENT_IMMA_MMA_SYNC (1 << 16)
 
+/* Which tensor-core kernel an IMMA-flavour convolution of `rows` streams
+ * (fused extract when `extract`) with K taps runs: 2 = tcgen05, 1 = mma.sync,
+ * 0 = not an IMMA flavour. */
+int nent_imma_kernel(int flavor, int K, int rows, int extract);
+
 /* Elementwise op codes (ops.py:193-204). */
 #define NENT_EW_ADD 0
 #define NENT_EW_SUB 1
@@ -245,9 +250,11 @@ int nent_copy_rows(void *dst, int64_t dst_pitch, const void *src, int64_t src_pi
 /* ---- measurement ------------------------------------------------------------ */
 
 #define NENT_BENCH_IMMA 16 /* microbenchmark only: mma.sync m16n8k32 s8 (legacy IMMA) */
+#define NENT_BENCH_TC05 17 /* microbenchmark only: tcgen05.mma kind::i8 128x128x32, A in TMEM */
 
 /* Integer / FP64 pipe microbenchmark used for the roofline denominators.
- * kind: NENT_MAC_* flavour or NENT_BENCH_IMMA; launches blocks x threads threads each doing
+ * kind: NENT_MAC_* flavour, NENT_BENCH_IMMA or NENT_BENCH_TC05 (one CTA of 128 threads per block,
+ * `iters` chains of 12 MMAs; `threads` ignored); otherwise launches blocks x threads threads each doing
  * `iters` x 16 independent MACs; sink_dev receives a value so nothing is
  * dead-code eliminated. Returns MACs issued via *macs_out (host). */
 int nent_microbench(int kind, int blocks, int threads, int iters, unsigned long long *sink_dev,

@@ -255,6 +255,12 @@ def chain_conv(a: torch.Tensor | None, b: torch.Tensor, g_dev: torch.Tensor, K: 
     return out
 
 
+def imma_kernel(flavor: int, K: int, rows: int, extract: bool) -> str:
+    """Which tensor-core kernel an IMMA flavour runs for this shape."""
+    return {0: "cuda-core", 1: "mma.sync", 2: "tcgen05"}[
+        _lib.lib().nent_imma_kernel(int(flavor), int(K), int(rows), int(bool(extract)))]
+
+
 def copy_rows(dst: torch.Tensor, src: torch.Tensor) -> None:
     """dst[:] = src for two (rows, width) views with contiguous rows and any
     row pitch, one on the device and one in pinned host memory (or both on

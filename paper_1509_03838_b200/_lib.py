@@ -19,6 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libnent_b200.so"
 NENT_OK, NENT_ERR_PARAM, NENT_ERR_RANGE, NENT_ERR_CUDA, NENT_ERR_OVERFLOW = 0, 1, 2, 3, 4
 MAC_I32, MAC_F64, MAC_W64, MAC_S64, MAC_G64, MAC_X128, MAC_IMMA = 1, 2, 3, 4, 5, 6, 7
 BENCH_IMMA = 16
+BENCH_TC05 = 17
 
 
 IMMA_MMA_SYNC = 1 << 16  # NENT_IMMA_MMA_SYNC: force the mma.sync kernel
@@ -43,7 +44,7 @@ class _FlavorNames(dict):
 
 
 MAC_NAMES = _FlavorNames({MAC_I32: "i32", MAC_F64: "f64", MAC_W64: "w64", MAC_S64: "s64",
-                          MAC_G64: "g64", MAC_X128: "x128", BENCH_IMMA: "imma_s8_mma_sync"})
+                          MAC_G64: "g64", MAC_X128: "x128", BENCH_IMMA: "imma_s8_mma_sync", BENCH_TC05: "tcgen05_i8"})
 EW_ADD, EW_SUB, EW_MUL = 0, 1, 2
 
 _P = ctypes.c_void_p
@@ -82,6 +83,7 @@ SIGNATURES = {
     "nent_check_range": [_PP, _I, _I, _L, _L, _P, _P],
     "nent_checksum_encode": [_PP, _I, _I, _L, _P, _I, _P],
     "nent_checksum_recover": [_PP, _I, _P, _I, _I, _L, _I, _P, _I, _P],
+    "nent_imma_kernel": [_I, _I, _I, _I],
     "nent_copy_rows": [_P, _L, _P, _L, _L, _I, _I, _P],
     "nent_microbench": [_I, _I, _I, _I, _P, ctypes.POINTER(ctypes.c_double), _P],
 }

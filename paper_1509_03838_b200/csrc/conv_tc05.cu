@@ -615,30 +615,39 @@ static int sm_count_tc() {
 
 // Returns NENT_TC05_NA when the shape is outside this kernel's envelope (the
 // caller then runs the mma.sync kernel), else a NENT status.
-int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
+// Geometry of the tcgen05 kernel for K taps, or false when the shape is
+// outside its envelope (m != 3 fused, > 64 rows, K > 257, np > 6, taps wider
+// than their 192 TMEM columns, class sums that could leave int32).
+static bool tc05_geometry(int K, int rows, int np, int ng, bool extract, tcc::Geom& G, size_t& smem) {
   using namespace tcc;
-  if (extract ? A.rows != 3 : A.rows > NENT_MAX_STREAMS) return NENT_TC05_NA;
-  if (np < 1 || np > 8 || ng < 1 || ng > 4) return NENT_TC05_NA;
-  Geom G{};
-  G.KT = (A.K + 127 + 127) / 128 * 128;  // K steps in multiples of 4 (NSTEPS = 4, 8, 12)
+  if (extract ? rows != 3 : rows > NENT_MAX_STREAMS) return false;
+  if (np < 1 || np > 6 || ng < 1 || ng > 4) return false;
+  G = Geom{};
+  G.KT = (K + 127 + 127) / 128 * 128;  // K steps in multiples of 4 (NSTEPS = 4, 8, 12)
   G.nsteps = G.KT / 32;
-  if (G.nsteps > 12) return NENT_TC05_NA;
+  if (G.nsteps > 12) return false;
   G.natoms = (G.KT + 127) / 128;
-  if (8 * ng * G.nsteps > TAPCOLS) return NENT_TC05_NA;  // taps must fit their TMEM columns
+  if (8 * ng * G.nsteps > TAPCOLS) return false;  // taps must fit their TMEM columns
   G.np = np;
   G.ng = ng;
   G.ncls = np + ng - 1;
-  G.nstreams = A.rows;
-  { const char* e = getenv("NENT_TC05_DEBUG"); G.debug = e ? atoi(e) : 0; }
+  G.nstreams = rows;
   // every class accumulator is an exact int32: |sum| <= 2^14 K min(np, ng)
-  if ((int64_t)16384 * A.K * (np < ng ? np : ng) >= ((int64_t)1 << 31)) return NENT_TC05_NA;
+  if ((int64_t)16384 * K * (np < ng ? np : ng) >= ((int64_t)1 << 31)) return false;
   G.nw = (128 * U + G.KT - 128) / 4;
-  if (G.nw > 2 * HALFW * 32 * NPROD) return NENT_TC05_NA;
-  if (4 * G.nw > PLANE) return NENT_TC05_NA;
+  if (G.nw > 2 * HALFW * 32 * NPROD || 4 * G.nw > PLANE) return false;
   G.plane = PLANE;
   G.stage_off = 2 * np * PLANE;
-  const size_t smem = 1024 + (size_t)G.stage_off + (size_t)2 * HALFW * 2 * 32 * NPROD * 16;
-  if (smem > 227 * 1024) return NENT_TC05_NA;
+  smem = 1024 + (size_t)G.stage_off + (size_t)2 * HALFW * 2 * 32 * NPROD * 16;
+  return smem <= 227 * 1024 && sm_count_tc() > 0;
+}
+
+int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
+  using namespace tcc;
+  Geom G;
+  size_t smem = 0;
+  if (!tc05_geometry(A.K, A.rows, np, ng, extract, G, smem)) return NENT_TC05_NA;
+  { const char* e = getenv("NENT_TC05_DEBUG"); G.debug = e ? atoi(e) : 0; }
   const int sms = sm_count_tc();
   if (sms <= 0) return NENT_TC05_NA;
   G.ntiles = (A.n_out + TILE - 1) / TILE;
@@ -650,7 +659,6 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
   static const KernFn table[2][3][6] = {{TC05_ROW(false, 4), TC05_ROW(false, 8), TC05_ROW(false, 12)},
                                         {TC05_ROW(true, 4), TC05_ROW(true, 8), TC05_ROW(true, 12)}};
 #undef TC05_ROW
-  if (np > 6) return NENT_TC05_NA;
   const int si = G.nsteps / 4 - 1;
   const KernFn kern = table[extract][si][np - 1];
   static size_t configured[2][3][6] = {};
@@ -681,3 +689,13 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
 }
 
 }  // namespace nent
+
+using namespace nent;
+
+extern "C" int nent_imma_kernel(int flavor, int K, int rows, int extract) {
+  if ((flavor & 0xff) != NENT_MAC_IMMA) return 0;
+  if (flavor & NENT_IMMA_MMA_SYNC) return 1;
+  tcc::Geom G;
+  size_t smem = 0;
+  return tc05_geometry(K, rows, (flavor >> 8) & 0xf, (flavor >> 12) & 0xf, extract != 0, G, smem) ? 2 : 1;
+}

@@ -5,6 +5,7 @@
 // 16 independent accumulators per thread keep the pipe saturated and the count
 // of issued MACs exact.
 #include "common.cuh"
+#include "tc05.cuh"
 
 namespace nent {
 
@@ -107,6 +108,56 @@ __global__ void __launch_bounds__(256) microbench_imma_kernel(int iters, unsigne
   if (s == (unsigned long long)k * 0x9e3779b97f4a7c15ull) sink[tid & 1023] = s;
 }
 
+// 5th-generation tensor cores: tcgen05.mma kind::i8, M=128 x N=128 x K=32 per
+// instruction, A from TMEM, B from shared memory, one CTA per SM, the elected
+// lane of warp 0 issuing 12-step K chains back to back (the conv kernel's
+// issue shape at its largest N).  Operand contents are irrelevant to timing.
+__global__ void __launch_bounds__(128, 1) microbench_tc05_kernel(int iters, unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t mbar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tc05::alloc(&tslot, 512);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc05::smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 128 * 128 + 512; i += blockDim.x) smem[i] = (unsigned char)(i * 7 + 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc05::fence_before();
+  __syncthreads();
+  tc05::fence_after();
+  const uint32_t tbase = tslot;
+  if (warp == 0) {
+    const uint32_t idesc = tc05::idesc_i8(128, 128, false);
+    const uint32_t blo = tc05::desc_sw128_lo(tc05::smem_u32(smem));
+    for (int it = 0; it < iters; ++it) {
+      uint32_t e;
+      asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(e));
+      if (e) {
+#pragma unroll
+        for (int kc = 0; kc < 12; ++kc) tc05::mma_i8_ts_lo(tbase + 128, tbase + 8u * kc, blo + 2u * kc, idesc, 1u);
+      }
+      __syncwarp();
+    }
+    tc05::commit_elect(tc05::smem_u32(&mbar));
+    asm volatile(
+        "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W_%=;\n}" ::"r"(
+            tc05::smem_u32(&mbar))
+        : "memory");
+  }
+  tc05::fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc05::fence_after();
+    uint32_t r[16];
+    tc05::ld_x16(tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 128, r);
+    tc05::wait_ld();
+    if (r[0] == 0x12345678u && r[1] == 0x9abcdef0u) sink[blockIdx.x & 1023] = r[2];
+    tc05::dealloc(tbase, 512);
+  }
+}
+
 }  // namespace nent
 
 using namespace nent;
@@ -130,6 +181,13 @@ extern "C" int nent_microbench(int kind, int blocks, int threads, int iters,
       microbench_imma_kernel<<<blocks, threads, 0, s>>>(iters, sink_dev, k);
       per_thread = (double)iters * MB_CHAINS * (16.0 * 8 * 32 / 32);  // 4096 MACs per warp-MMA
       break;
+    case NENT_BENCH_TC05: {
+      const int smem = 128 * 128 + 512 + 1024;
+      cudaFuncSetAttribute(microbench_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      microbench_tc05_kernel<<<blocks, 128, smem, s>>>(iters, sink_dev);
+      if (macs_out) *macs_out = (double)iters * 12 * 128.0 * 128.0 * 32.0 * (double)blocks;
+      return check_launch("microbench tc05");
+    }
     default: set_error("microbench: unknown kind %d", kind); return NENT_ERR_PARAM;
   }
   if (macs_out) *macs_out = per_thread * (double)blocks * (double)threads;

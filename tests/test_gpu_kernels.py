@@ -148,6 +148,8 @@ def test_tcgen05_and_mma_sync_kernels(oracle, K, bits):
         fl = imma_flavor(D.signed_digits(lim), D.signed_digits(lim), mma_sync)
         y, _ = D.conv(xd, D.taps_tensor(g, fl), K, fl, period=n + K - 1)
         assert np.array_equal(y.cpu().numpy(), ref), ("plain", K, bits, mma_sync)
+        if lim * lim * K >= nent.output_range(p).hi:
+            continue  # outputs outside the codec's admitted range: recovery undefined
         fl = imma_flavor(D.signed_digits(lim * ((1 << p.l) + 1)), D.signed_digits(lim), mma_sync)
         for r in (None, 0, 1, 2):
             res = fused.entangled_conv(nent.StreamBlock(p, xd), g, failed=r, flavor=fl)

@@ -29,9 +29,10 @@
 //   warps 1-3   producers: cp.async global -> smem staging (one half-stream
 //               ahead), entangle, digit split -> planes (2 stream slots)
 //   warps 4-11  epilogue: TMEM -> int64 classes -> recovery -> coalesced stores
-// TMEM (512 columns): [0,192) taps, [192,320) stash of the first stream's
-// int64 result until the second arrives, [320,512) a ring of 3 accumulator
-// slots of U=64 columns.  mbarriers hand plane slots and accumulator slots
+// TMEM (512 columns): [0,192) taps, [192,512) a ring of 5 accumulator slots
+// of U=64 columns.  Shared memory: two plane slots, the cp.async staging, and
+// the stash of the first stream's int64 result until the second arrives (and
+// of the check word until the redundant stream arrives).  mbarriers hand plane slots and accumulator slots
 // between the roles (tcgen05.commit arrives when the MMAs reading / writing
 // them are done).
 #include "common.cuh"
@@ -51,13 +52,14 @@ constexpr int NPROD = 3;         // producer warps (12 warps in all: 3 per SM su
 constexpr int NEPI = 8;          // epilogue warps (two per TMEM lane quadrant)
 constexpr int NT = 32 * (1 + NPROD + NEPI);
 constexpr int TAPCOLS = 192;     // TMEM columns for the tap table (8 per digit and K step)
-constexpr int STASH = TAPCOLS;   // first stash column (128 columns)
-constexpr int RING0 = STASH + 128;
-constexpr int SLOTS = (512 - RING0) / U;  // accumulator ring: 3 slots of U columns
-constexpr int HALFW = 12;        // staged words per producer thread and half-stream
+constexpr int RING0 = TAPCOLS;
+constexpr int SLOTS = (512 - RING0) / U;  // accumulator ring: 5 slots of U columns (the
+                                          // MMA runs up to 4 classes ahead of the epilogue)
+constexpr int HALFW = 11;        // staged words per producer thread and half-stream
 constexpr int PLANE = 9216;      // bytes per digit plane: 128*U + KT - 128 <= 9216, 1024-aligned
-constexpr int NWP = 2 * HALFW * 32 * NPROD;  // plane words every fast tile fills (2304 = PLANE / 4)
-static_assert(4 * NWP == PLANE, "staging covers exactly one plane");
+constexpr int NWP = 2 * HALFW * 32 * NPROD;  // plane words every fast tile fills (2112)
+static_assert(4 * NWP <= PLANE, "staging fits one plane");
+constexpr int STASH_BYTES = 32 * NEPI * 32 * 8;  // 32 int64 per epilogue thread
 
 struct Geom {
   int KT;         // GEMM K: K + 127 rounded up to 32
@@ -68,6 +70,7 @@ struct Geom {
   int nw;         // 32-bit plane words per stream and tile
   int plane;      // bytes per digit plane, 1024-aligned
   int stage_off;  // smem offset of the cp.async staging (planes at 0)
+  int stash_off;  // smem offset of the epilogue stash
   int64_t ntiles;
   int debug;      // profiling only: 1 skip producer math, 2 skip epilogue math, 4 skip MMAs, 8 role timers
   unsigned long long* dbg;  // role timers (debug & 8)
@@ -120,6 +123,14 @@ __device__ __forceinline__ uint32_t byte_col(uint32_t w0, uint32_t w1, uint32_t 
 // still interleave)
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(v));
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ int4 lds128(uint32_t addr) {
   int4 r;
@@ -325,7 +336,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
               const int rs = k % SLOTS;
               const int use = k / SLOTS;
               const bool first = p == (c - G.ng + 1 > 0 ? c - G.ng + 1 : 0);
-              if (first && use >= 1) {
+              if (first && use >= 1 && !(G.debug & 64)) {
                 TC05_TIMED(1, mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1)));
                 tc05::fence_after();
               }
@@ -366,7 +377,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
       row = stream_of(q, EXTRACT, pivot, A.rows);
     };
     auto issue = [&](int64_t H) {
-      if (H < units) {
+      if (H < units && !(G.debug & 32)) {
         int64_t P0;
         int row, h, q;
         unit(H, P0, row, h, q);
@@ -435,7 +446,9 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     const int quad = warp & 3, half = ew >> 2;
     const uint32_t lrow = (uint32_t)(32 * quad) << 16;
     const int v = 32 * quad + lane;
-    const uint32_t stash = tbase + lrow + (uint32_t)(STASH + 64 * half);
+    // thread-private stash, [i][epilogue thread] int64: coalesced, conflict-free
+    const uint32_t stash = planes_s + (uint32_t)G.stash_off + 8u * (uint32_t)(32 * ew + lane);
+    constexpr uint32_t SSTEP = 8u * 32 * NEPI;
     // the unsigned B digits carry +128 each: every output is high by
     // 128 * sum(g) * sum_{p<NP} 256^p (mod 2^64); start the sums at minus that
     uint64_t gsum = 0;
@@ -454,40 +467,38 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
         uint64_t acc[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc[i] = corr;
-        for (int c = 0; c < G.ncls; ++c) {
-          const int64_t k = cls + c;
-          const int rs = (int)(k % SLOTS);
-          TC05_TIMED(0, mb_wait(accf_b(rs), (uint32_t)((k / SLOTS) & 1)));
-          tc05::fence_after();
-          uint32_t r0[16], r1[16];
-          const uint32_t col = tbase + lrow + (uint32_t)(RING0 + rs * U + 32 * half);
-          if (!(G.debug & 16)) {
-            tc05::ld_x16(col, r0);
-            tc05::ld_x16(col + 16, r1);
-            tc05::wait_ld();
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) r0[i] = r1[i] = 0;
-          }
-          tc05::fence_before();
-          __syncwarp();
-          if (lane == 0) mb_arrive(acce_b(rs));
-          if (G.debug & 2) {
-          } else if (c < 4) {  // acc += A * 256^c: one IMAD.WIDE
+        // acc += A_c * 256^c (IMAD.WIDE; for c >= 4 only the high word moves)
+        auto accum = [&](int c, const uint32_t (&r)[32]) {
+          if (G.debug & 2) return;
+          if (c < 4) {
             const int32_t mul = 1 << (8 * c);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              acc[i] = mad_wide(r0[i], mul, acc[i]);
-              acc[16 + i] = mad_wide(r1[i], mul, acc[16 + i]);
-            }
-          } else {  // 256^c >= 2^32: only the high word moves
+            for (int i = 0; i < 32; ++i) acc[i] = mad_wide(r[i], mul, acc[i]);
+          } else {
             const int32_t mul = 1 << (8 * (c - 4));
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              acc[i] = mad_hi_word(r0[i], mul, acc[i]);
-              acc[16 + i] = mad_hi_word(r1[i], mul, acc[16 + i]);
-            }
+            for (int i = 0; i < 32; ++i) acc[i] = mad_hi_word(r[i], mul, acc[i]);
           }
+        };
+        // classes two at a time: one TMEM round trip (wait::ld) per pair
+        for (int c = 0; c < G.ncls; c += 2) {
+          const bool two = c + 1 < G.ncls;
+          const int k0 = (int)(cls + c), rs0 = k0 % SLOTS, rs1 = (k0 + 1) % SLOTS;
+          TC05_TIMED(0, mb_wait(accf_b(rs0), (uint32_t)((k0 / SLOTS) & 1)));
+          if (two) TC05_TIMED(0, mb_wait(accf_b(rs1), (uint32_t)(((k0 + 1) / SLOTS) & 1)));
+          tc05::fence_after();
+          uint32_t r0[32], r1[32];
+          tc05::ld_x32(tbase + lrow + (uint32_t)(RING0 + rs0 * U + 32 * half), r0);
+          if (two) tc05::ld_x32(tbase + lrow + (uint32_t)(RING0 + rs1 * U + 32 * half), r1);
+          tc05::wait_ld();
+          tc05::fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mb_arrive(acce_b(rs0));
+            if (two) mb_arrive(acce_b(rs1));
+          }
+          accum(c, r0);
+          if (two) accum(c + 1, r1);
         }
         if (!EXTRACT) {
           void* yp = A.y.p[q];
@@ -504,69 +515,40 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             for (int i = 0; i < 32; ++i)
               if (128 * i < lim) yo[128 * i] = (int64_t)acc[i];
           }
-        } else if (q == 0) {  // delta_{pivot+1}: park it in TMEM
+        } else if (q == 0) {  // delta_{pivot+1}: park it in shared memory
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            uint32_t w[16];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              w[2 * i] = (uint32_t)acc[8 * h + i];
-              w[2 * i + 1] = (uint32_t)(acc[8 * h + i] >> 32);
-            }
-            st_x16(stash + 16 * h, w);
-          }
-          tc05::wait_st();
+          for (int i = 0; i < 32; ++i) sts64(stash + SSTEP * i, acc[i]);
         } else if (q == 1) {  // delta_{pivot+2}: recover all three, store, park the check word
           void* y0 = A.y.p[pivot];
           void* y1 = A.y.p[pivot + 1 >= 3 ? pivot - 2 : pivot + 1];
           void* y2 = A.y.p[pivot + 2 >= 3 ? pivot - 1 : pivot + 2];
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            uint32_t w[16];
-            tc05::ld_x16(stash + 16 * h, w);
-            tc05::wait_ld();
-            uint32_t chk[16];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int ii = 8 * h + i;
-              int64_t rot[3], orot[3];
-              rot[0] = (int64_t)(((uint64_t)w[2 * i + 1] << 32) | w[2 * i]);
-              rot[1] = (int64_t)acc[ii];
-              rot[2] = 0;
-              recover_rot_valid<3>(rot, A.l, orot);
-              const int64_t o = ybase + 128 * (32 * half + ii) + v;
-              if (o < A.n_out) {
-                if (A.y_bits == 32) {
-                  reinterpret_cast<int32_t*>(y0)[o] = (int32_t)orot[0];
-                  reinterpret_cast<int32_t*>(y1)[o] = (int32_t)orot[1];
-                  reinterpret_cast<int32_t*>(y2)[o] = (int32_t)orot[2];
-                } else {
-                  reinterpret_cast<int64_t*>(y0)[o] = orot[0];
-                  reinterpret_cast<int64_t*>(y1)[o] = orot[1];
-                  reinterpret_cast<int64_t*>(y2)[o] = orot[2];
-                }
+          for (int i = 0; i < 32; ++i) {
+            int64_t rot[3], orot[3];
+            rot[0] = (int64_t)lds64(stash + SSTEP * i);
+            rot[1] = (int64_t)acc[i];
+            rot[2] = 0;
+            recover_rot_valid<3>(rot, A.l, orot);
+            const int64_t o = ybase + 128 * (32 * half + i) + v;
+            if (o < A.n_out) {
+              if (A.y_bits == 32) {
+                reinterpret_cast<int32_t*>(y0)[o] = (int32_t)orot[0];
+                reinterpret_cast<int32_t*>(y1)[o] = (int32_t)orot[1];
+                reinterpret_cast<int32_t*>(y2)[o] = (int32_t)orot[2];
+              } else {
+                reinterpret_cast<int64_t*>(y0)[o] = orot[0];
+                reinterpret_cast<int64_t*>(y1)[o] = orot[1];
+                reinterpret_cast<int64_t*>(y2)[o] = orot[2];
               }
-              // the pivot stream's word must equal (d_{pivot-1} << l) + d_pivot
-              const uint64_t e = (uint64_t)wadd(wshl(orot[2], A.l), orot[0]);
-              chk[2 * i] = (uint32_t)e;
-              chk[2 * i + 1] = (uint32_t)(e >> 32);
             }
-            if (A.r < 0) st_x16(stash + 16 * h, chk);
+            // the pivot stream's word must equal (d_{pivot-1} << l) + d_pivot
+            if (A.r < 0) sts64(stash + SSTEP * i, (uint64_t)wadd(wshl(orot[2], A.l), orot[0]));
           }
-          tc05::wait_st();
         } else if (A.r < 0) {  // q == 2, verify: the redundant stream against the recovery
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            uint32_t w[16];
-            tc05::ld_x16(stash + 16 * h, w);
-            tc05::wait_ld();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int ii = 8 * h + i;
-              const uint64_t e = ((uint64_t)w[2 * i + 1] << 32) | w[2 * i];
-              const int64_t o = ybase + 128 * (32 * half + ii) + v;
-              if (o < A.n_out && e != acc[ii]) ++bad;
-            }
+          for (int i = 0; i < 32; ++i) {
+            const int64_t o = ybase + 128 * (32 * half + i) + v;
+            if (o < A.n_out && lds64(stash + SSTEP * i) != acc[i]) ++bad;
           }
         }
       }
@@ -638,7 +620,8 @@ static bool tc05_geometry(int K, int rows, int np, int ng, bool extract, tcc::Ge
   if (G.nw > 2 * HALFW * 32 * NPROD || 4 * G.nw > PLANE) return false;
   G.plane = PLANE;
   G.stage_off = 2 * np * PLANE;
-  smem = 1024 + (size_t)G.stage_off + (size_t)2 * HALFW * 2 * 32 * NPROD * 16;
+  G.stash_off = G.stage_off + 2 * HALFW * 2 * 32 * NPROD * 16;
+  smem = (size_t)G.stash_off + (extract ? STASH_BYTES : 0);
   return smem <= 227 * 1024 && sm_count_tc() > 0;
 }
 

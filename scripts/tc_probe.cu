@@ -195,16 +195,37 @@ template <int VARIANT>
 __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycles, unsigned long long* sink, int nsteps_rt) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
-  __shared__ __align__(8) uint64_t mbar, mbar2;
+  __shared__ __align__(8) uint64_t mbar, mbar2, accf[3], acce[3];
   __shared__ int stop_flag;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) tc05::alloc(&tslot, 512);
   if (tid == 0) {
     mbar_init(tc05::smem_u32(&mbar));
     mbar_init(tc05::smem_u32(&mbar2));
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(tc05::smem_u32(&accf[i]));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tc05::smem_u32(&acce[i])));
+    }
     stop_flag = 0;
   }
-  for (int i = tid; i < 2 * 5 * 9216; i += blockDim.x) smem[i] = (unsigned char)(i * 7);
+  for (int i = tid; i < 2 * 5 * 9216; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    h ^= h >> 15;
+    smem[i] = VARIANT == 7 ? (unsigned char)(h * 0x2c1b3c6du >> 24) : (unsigned char)(i * 7);
+  }
+  if (VARIANT == 7 && warp < 4) {  // random taps in TMEM columns [0, 192)
+    for (int blk = 0; blk < 24; ++blk) {
+      uint32_t w[8];
+      for (int c = 0; c < 8; ++c) {
+        uint32_t h = (uint32_t)(tid * 977 + blk * 131 + c) * 2654435761u;
+        h ^= h >> 13;
+        w[c] = h * 0x85ebca6bu;
+      }
+      tc05::st_x8(((uint32_t)(32 * warp) << 16) + 8u * blk, w);
+    }
+    tc05::wait_st();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc05::fence_before();
   __syncthreads();
   tc05::fence_after();
@@ -218,8 +239,12 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
       for (int p = 0; p < 5; ++p) {
         const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * 5 + p) * 9216));
         for (int j = 0; j < 2; ++j) {
-          const int c = p + j, k = cls + c, rs = k % 3;
+          const int c = p + j, k = cls + c, rs = k % 3, use = k / 3;
           const bool first = p == (c - 1 > 0 ? c - 1 : 0);
+          if ((VARIANT == 8 || VARIANT == 9) && first && use >= 1) {
+            mbar_wait(tc05::smem_u32(&acce[rs]), (use - 1) & 1);
+            tc05::fence_after();
+          }
           const uint32_t d = 320u + 64u * rs, a = 96u * j;
           if (VARIANT == 6) {  // runtime step count in chunks of 4 (KT padded to 128)
             if (elect_one_probe()) {
@@ -238,7 +263,7 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
                   tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
             }
             __syncwarp();
-          } else if (VARIANT == 0) {
+          } else if (VARIANT == 0 || VARIANT == 7 || VARIANT == 8 || VARIANT == 9) {
             if (elect_one_probe()) {
 #pragma unroll
               for (int kc = 0; kc < 12; ++kc) tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
@@ -251,7 +276,7 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
             }
             __syncwarp();
           }
-          if (p == (c < 4 ? c : 4)) tc05::commit_elect(tc05::smem_u32(&mbar2));
+          if (p == (c < 4 ? c : 4)) tc05::commit_elect(tc05::smem_u32((VARIANT == 8 || VARIANT == 9) ? &accf[rs] : &mbar2));
         }
       }
     }
@@ -261,6 +286,36 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
       *cycles = clock64() - t0;
       stop_flag = 1;
     }
+  } else if ((VARIANT == 8 || VARIANT == 9) && warp >= 4) {
+    unsigned long long acc = tid;
+    const int half = (warp - 4) >> 2;
+    for (int k = 0; k < streams * 6; ++k) {
+      const int rs = k % 3;
+      mbar_wait(tc05::smem_u32(&accf[rs]), (k / 3) & 1);
+      tc05::fence_after();
+      uint32_t r[32];
+      tc05::ld_x32(((uint32_t)(32 * (warp & 3)) << 16) + 320u + 64u * rs + 32u * half, r);
+      tc05::wait_ld();
+      tc05::fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc05::smem_u32(&acce[rs])) : "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc += r[i];
+      if (VARIANT == 9) {  // epilogue-like work: 32 IMAD.WIDE and 32 coalesced 4-byte stores per class
+        unsigned long long a2 = acc;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          long long d;
+          asm volatile("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(r[i]), "r"(i + 3), "l"((long long)a2));
+          a2 = (unsigned long long)d;
+        }
+        unsigned* out = reinterpret_cast<unsigned*>(sink) + 4096 + (size_t)blockIdx.x * 65536;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) out[(k & 7) * 8192 + 256 * i + (tid - 128)] = (unsigned)(a2 >> (i & 31));
+        acc ^= a2;
+      }
+    }
+    if (acc == 42) *sink = acc;
   } else if (warp >= 4) {
     unsigned long long acc = tid;
     uint32_t r[16];
@@ -297,7 +352,7 @@ void run_convlike() {
   cudaFuncSetAttribute(convlike<VARIANT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int streams = 42;
   unsigned long long* sink;
-  cudaMalloc(&sink, 8);
+  cudaMalloc(&sink, (size_t)8 * (512 + 148 * 32768));
   convlike<VARIANT><<<148, 384, smem>>>(streams, dc, sink, 12);
   cudaDeviceSynchronize();
   long long cyc;
@@ -309,6 +364,9 @@ void run_convlike() {
 
 int main() {
   run_convlike<0>();
+  run_convlike<8>();
+  run_convlike<9>();
+  run_convlike<7>();
   run_convlike<5>();
   run_convlike<6>();
   run_convlike<2>();

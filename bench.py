@@ -188,18 +188,19 @@ def run_ours(args):
     params, c_np, g = make_inputs(rank, n, K)
     m, H = params.m, K - 1
     c_dev = torch.from_numpy(c_np).to(dev).to(torch.int32)
-    if world > 1:  # halo-split: the K-1 samples left of this rank's slice come from rank-1
-        halo = torch.zeros((m, H), dtype=torch.int32, device=xdev)
+    if world > 1:  # halo-split: the samples left of this rank's slice come from rank-1
+        Hp = (H + 3) // 4 * 4  # K-1 rounded up to 4 words: the kernel's tiles then start 16-byte aligned
+        halo = torch.zeros((m, Hp), dtype=torch.int32, device=xdev)
         ops = []
         if rank + 1 < world:
-            ops.append(dist.P2POp(dist.isend, c_dev[:, n - H:].contiguous().to(xdev), rank + 1))
+            ops.append(dist.P2POp(dist.isend, c_dev[:, n - Hp:].contiguous().to(xdev), rank + 1))
         if rank > 0:
             ops.append(dist.P2POp(dist.irecv, halo, rank - 1))
         for w in dist.batch_isend_irecv(ops):
             w.wait()
         x_dev = torch.cat([halo.to(dev), c_dev], dim=1).contiguous()
         n_out = n + (H if rank == world - 1 else 0)  # the last rank also owns the K-1 tail
-        period, n_in, y_begin = H + n + H, H + n, H  # rank 0 keeps a zero halo (left edge)
+        period, n_in, y_begin = Hp + n + H, Hp + n, Hp  # rank 0 keeps a zero halo (left edge)
     else:
         x_dev = c_dev
         n_out, period, n_in, y_begin = n + H, n + H, n, 0

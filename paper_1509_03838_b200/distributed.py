@@ -217,11 +217,19 @@ class HaloSplit:
         if self.compute is None:
             self.compute = DeviceCompute()
 
+    @property
+    def halo_width(self) -> int:
+        """K-1 rounded up to 4 samples, so the fused kernel's tiles start on
+        16-byte boundaries of the [halo | slice] rows."""
+        return (self.K - 1 + 3) // 4 * 4
+
     def exchange_halo(self, c_slice: torch.Tensor) -> torch.Tensor:
-        """[halo | slice]: the K-1 samples left of this slice, from rank-1
-        (zeros on rank 0, the signal's left edge)."""
-        H = self.K - 1
+        """[halo | slice]: the halo_width samples left of this slice, from
+        rank-1 (zeros on rank 0, the signal's left edge)."""
+        H = self.halo_width
         m = c_slice.shape[0]
+        if H > c_slice.shape[1]:
+            raise ValueError(f"slice of {c_slice.shape[1]} samples is shorter than the halo ({H})")
         halo = c_slice.new_zeros((m, H))
         if H and self.world > 1:
             ops = []
@@ -238,13 +246,13 @@ class HaloSplit:
         """Recovered full-convolution outputs owned by this rank: positions
         [start, start + n_slice) of the global output (+ the K-1 tail on the
         last rank)."""
-        H = self.K - 1
+        H, Hp = self.K - 1, self.halo_width
         x = self.exchange_halo(c_slice)
         n = c_slice.shape[1]
         last = self.rank == self.world - 1
         n_out = n + (H if last else 0)
-        return self.compute.fused_conv(x, self.params, g, period=n + 2 * H, n_in=n + H,
-                                       y_begin=H, n_out=n_out, failed=failed)
+        return self.compute.fused_conv(x, self.params, g, period=Hp + n + H, n_in=Hp + n,
+                                       y_begin=Hp, n_out=n_out, failed=failed)
 
     def gather(self, d_local: torch.Tensor, dst: int = 0):
         sizes = torch.tensor([d_local.shape[1]], dtype=torch.int64)

@@ -64,14 +64,17 @@ class ChunkedEntangledConv:
         self.dev = device or D.device()
         self.g_dev = D.taps_tensor(self.g, flavor)
         m, H = params.m, self.K - 1
-        self.table = D.imma_table(self.g_dev, self.K, flavor, y_begin=H)  # every chunk's window starts at H
+        # every chunk's input window starts HP = K-1 rounded up to 4 samples before
+        # its first output, so the kernel's tiles start on 16-byte boundaries
+        self.HP = (H + 3) // 4 * 4
+        self.table = D.imma_table(self.g_dev, self.K, flavor, y_begin=self.HP)
         self.s_in = torch.cuda.Stream(device=self.dev)
         self.s_comp = torch.cuda.Stream(device=self.dev)
         self.s_out = torch.cuda.Stream(device=self.dev)
         if not 0 <= lag < nbuf:
             raise ParameterError(f"lag {lag} must be in [0, nbuf)")
         self.nbuf, self.lag = nbuf, lag
-        row = (PRE + LEAD + self.chunk + H + 31) // 32 * 32  # 128-byte row starts
+        row = (PRE + LEAD + self.chunk + self.HP + 31) // 32 * 32  # 128-byte row starts
         self.xbuf = [torch.empty((m, row), dtype=in_dtype, device=self.dev) for _ in range(nbuf)]
         self.ybuf = [torch.empty((m, LEAD + self.chunk), dtype=out_dtype, device=self.dev)
                      for _ in range(nbuf)]
@@ -127,7 +130,7 @@ class ChunkedEntangledConv:
         Call ``synchronize()`` before reading ``d_host``."""
         if not c_host.is_pinned() or not d_host.is_pinned():
             raise ParameterError("host buffers must be pinned (torch.empty(..., pin_memory=True))")
-        m, H, n, L = self.p.m, self.K - 1, self.n, self.L
+        m, H, n, L = self.p.m, self.HP, self.n, self.L
         if tuple(c_host.shape) != (m, n) or tuple(d_host.shape) != (m, L):
             raise ParameterError(f"expected c_host {(m, n)} and d_host {(m, L)}")
         if c_host.stride(1) != 1 or d_host.stride(1) != 1:

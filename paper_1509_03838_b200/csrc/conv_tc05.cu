@@ -72,6 +72,7 @@ struct Geom {
   int stage_off;  // smem offset of the cp.async staging (planes at 0)
   int stash_off;  // smem offset of the epilogue stash
   int64_t ntiles;
+  int shift;      // tiles start `shift` outputs before y_begin so input windows are 16-byte aligned
   int debug;      // profiling only: 1 skip producer math, 2 skip epilogue math, 4 skip MMAs, 8 role timers
   unsigned long long* dbg;  // role timers (debug & 8)
 };
@@ -204,11 +205,15 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
+__device__ __forceinline__ void cp_async4_zfill(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
 // How a tile's input window is staged: 1 = every word in range (plain
 // cp.async), 2 = partly outside [0, n_in) in full (zero-padded) mode
-// (cp.async with zero fill), 0 = per element through conv_prologue (scale /
-// add / gather chains, circular wrap, 64-bit or unaligned rows).  Words never
-// straddle 0: P0 is a multiple of 4 whenever the row base is 16-byte aligned.
+// (cp.async with zero fill; words straddling 0 or n_in element by element),
+// 0 = per element through conv_prologue (scale / add / gather chains,
+// circular wrap, 64-bit rows, rows whose 16-byte phase differs from row 0's).
 __device__ __forceinline__ int tile_mode(const ConvArgs& A, int row, int64_t P0) {
   const int32_t* bp = reinterpret_cast<const int32_t*>(A.b.p[row]);
   const int32_t* ap = reinterpret_cast<const int32_t*>(A.a.p[row]);
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
       const int64_t lt = H / (2 * G.nstreams);
       q = (int)((H >> 1) % G.nstreams);
       h = (int)(H & 1);
-      P0 = A.y_begin + (blockIdx.x + lt * gridDim.x) * TILE - (G.KT - 128);
+      P0 = A.y_begin - G.shift + (blockIdx.x + lt * gridDim.x) * TILE - (G.KT - 128);
       row = stream_of(q, EXTRACT, pivot, A.rows);
     };
     auto issue = [&](int64_t H) {
@@ -395,10 +400,21 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
         } else if (mode == 2) {
           for (int i = 0; i < HALFW; ++i) {
             const int64_t q0 = P0 + 4 * (int64_t)(ptid + PT * (HALFW * h + i));
-            const int64_t left = A.n_in - q0;
-            const uint32_t nb = q0 < 0 || left <= 0 ? 0u : (left >= 4 ? 16u : (uint32_t)(4 * left));
-            cp_async16_zfill(st + (uint32_t)(2 * i * PT) * 16u, nb ? bp + q0 : bp, nb);
-            if (ap) cp_async16_zfill(st + (uint32_t)((2 * i + 1) * PT) * 16u, nb ? ap + q0 : ap, nb);
+            const uint32_t db = st + (uint32_t)(2 * i * PT) * 16u, da = st + (uint32_t)((2 * i + 1) * PT) * 16u;
+            if (q0 >= 0 && q0 + 4 <= A.n_in) {
+              cp_async16(db, bp + q0);
+              if (ap) cp_async16(da, ap + q0);
+            } else if (q0 + 4 <= 0 || q0 >= A.n_in) {
+              cp_async16_zfill(db, bp, 0);  // all four positions are zero padding
+              if (ap) cp_async16_zfill(da, ap, 0);
+            } else {  // straddles 0 or n_in: element by element
+              for (int e = 0; e < 4; ++e) {
+                const int64_t q = q0 + e;
+                const bool in = q >= 0 && q < A.n_in;
+                cp_async4_zfill(db + 4u * e, in ? bp + q : bp, in ? 4u : 0u);
+                if (ap) cp_async4_zfill(da + 4u * e, in ? ap + q : ap, in ? 4u : 0u);
+              }
+            }
           }
         }
       }
@@ -462,7 +478,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     unsigned bad = 0;
     int64_t cls = 0;
     for (int64_t tile = blockIdx.x; tile < G.ntiles; tile += gridDim.x) {
-      const int64_t ybase = tile * TILE;  // output index of (u=0, v=0)
+      const int64_t ybase = tile * TILE - G.shift;  // output index of (u=0, v=0)
       for (int q = 0; q < G.nstreams; ++q, cls += G.ncls) {
         uint64_t acc[32];
 #pragma unroll
@@ -500,20 +516,21 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           accum(c, r0);
           if (two) accum(c + 1, r1);
         }
-        if (!EXTRACT) {
+        if (G.debug & 128) {
+        } else if (!EXTRACT) {
           void* yp = A.y.p[q];
           const int64_t o0 = ybase + 128 * (32 * half) + v;
-          const int64_t lim = A.n_out - o0;  // element i is stored iff 128 i < lim
+          const int64_t lim = A.n_out - o0;  // element i is stored iff -o0 <= 128 i < lim
           if (A.y_bits == 32) {
             int32_t* yo = reinterpret_cast<int32_t*>(yp) + o0;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (128 * i < lim) yo[128 * i] = (int32_t)acc[i];
+              if (128 * i < lim && 128 * i + o0 >= 0) yo[128 * i] = (int32_t)acc[i];
           } else {
             int64_t* yo = reinterpret_cast<int64_t*>(yp) + o0;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (128 * i < lim) yo[128 * i] = (int64_t)acc[i];
+              if (128 * i < lim && 128 * i + o0 >= 0) yo[128 * i] = (int64_t)acc[i];
           }
         } else if (q == 0) {  // delta_{pivot+1}: park it in shared memory
 #pragma unroll
@@ -530,7 +547,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             rot[2] = 0;
             recover_rot_valid<3>(rot, A.l, orot);
             const int64_t o = ybase + 128 * (32 * half + i) + v;
-            if (o < A.n_out) {
+            if (o >= 0 && o < A.n_out) {
               if (A.y_bits == 32) {
                 reinterpret_cast<int32_t*>(y0)[o] = (int32_t)orot[0];
                 reinterpret_cast<int32_t*>(y1)[o] = (int32_t)orot[1];
@@ -548,7 +565,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int64_t o = ybase + 128 * (32 * half + i) + v;
-            if (o < A.n_out && lds64(stash + SSTEP * i) != acc[i]) ++bad;
+            if (o >= 0 && o < A.n_out && lds64(stash + SSTEP * i) != acc[i]) ++bad;
           }
         }
       }
@@ -633,7 +650,11 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
   { const char* e = getenv("NENT_TC05_DEBUG"); G.debug = e ? atoi(e) : 0; }
   const int sms = sm_count_tc();
   if (sms <= 0) return NENT_TC05_NA;
-  G.ntiles = (A.n_out + TILE - 1) / TILE;
+  {  // align the input windows: (row-0 word offset + P0) = 0 mod 4
+    const int64_t wb = (int64_t)((reinterpret_cast<uintptr_t>(A.b.p[0]) >> 2) & 3);
+    G.shift = (int)(((wb + A.y_begin - G.KT + 128) % 4 + 4) % 4);
+  }
+  G.ntiles = (A.n_out + G.shift + TILE - 1) / TILE;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
   using KernFn = void (*)(ConvArgs, Geom);
 #define TC05_ROW(E, S)                                                                                   \

@@ -191,18 +191,18 @@ void run_tput(int grid = 1) {
 // VARIANT 0: MMA warp alone; 2: + 8 warps of ALU work (IMAD.WIDE chains);
 // 3: + 8 warps streaming tcgen05.ld of the accumulator ring; 4: + 8 warps of
 // STS traffic to shared memory
-template <int VARIANT>
-__global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycles, unsigned long long* sink, int nsteps_rt) {
+template <int VARIANT, int NSL = 3>
+__global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycles, unsigned long long* sink, int nsteps_rt, int getenv_nowait) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
-  __shared__ __align__(8) uint64_t mbar, mbar2, accf[3], acce[3];
+  __shared__ __align__(8) uint64_t mbar, mbar2, accf[5], acce[5];
   __shared__ int stop_flag;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) tc05::alloc(&tslot, 512);
   if (tid == 0) {
     mbar_init(tc05::smem_u32(&mbar));
     mbar_init(tc05::smem_u32(&mbar2));
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 5; ++i) {
       mbar_init(tc05::smem_u32(&accf[i]));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tc05::smem_u32(&acce[i])));
     }
@@ -239,13 +239,13 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
       for (int p = 0; p < 5; ++p) {
         const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * 5 + p) * 9216));
         for (int j = 0; j < 2; ++j) {
-          const int c = p + j, k = cls + c, rs = k % 3, use = k / 3;
+          const int c = p + j, k = cls + c, rs = k % NSL, use = k / NSL;
           const bool first = p == (c - 1 > 0 ? c - 1 : 0);
           if ((VARIANT == 8 || VARIANT == 9) && first && use >= 1) {
             mbar_wait(tc05::smem_u32(&acce[rs]), (use - 1) & 1);
             tc05::fence_after();
           }
-          const uint32_t d = 320u + 64u * rs, a = 96u * j;
+          const uint32_t d = (NSL == 5 ? 192u : 320u) + 64u * rs, a = 96u * j;
           if (VARIANT == 6) {  // runtime step count in chunks of 4 (KT padded to 128)
             if (elect_one_probe()) {
               for (int k0 = 0; k0 < nsteps_rt; k0 += 4) {
@@ -290,11 +290,12 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
     unsigned long long acc = tid;
     const int half = (warp - 4) >> 2;
     for (int k = 0; k < streams * 6; ++k) {
-      const int rs = k % 3;
-      mbar_wait(tc05::smem_u32(&accf[rs]), (k / 3) & 1);
+      const int rs = k % NSL;
+      if (!getenv_nowait || (tid & 31) == 0) mbar_wait(tc05::smem_u32(&accf[rs]), (k / NSL) & 1);
+      __syncwarp();
       tc05::fence_after();
       uint32_t r[32];
-      tc05::ld_x32(((uint32_t)(32 * (warp & 3)) << 16) + 320u + 64u * rs + 32u * half, r);
+      tc05::ld_x32(((uint32_t)(32 * (warp & 3)) << 16) + (NSL == 5 ? 192u : 320u) + 64u * rs + 32u * half, r);
       tc05::wait_ld();
       tc05::fence_before();
       __syncwarp();
@@ -344,19 +345,20 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
   if (warp == 0) tc05::dealloc(tslot, 512);
 }
 
-template <int VARIANT>
+template <int VARIANT, int NSL = 3>
 void run_convlike() {
   long long* dc;
   cudaMalloc(&dc, 8);
   const int smem = 2 * 5 * 9216 + 8192;
-  cudaFuncSetAttribute(convlike<VARIANT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(convlike<VARIANT, NSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int streams = 42;
   unsigned long long* sink;
   cudaMalloc(&sink, (size_t)8 * (512 + 148 * 32768));
-  convlike<VARIANT><<<148, 384, smem>>>(streams, dc, sink, 12);
+  convlike<VARIANT, NSL><<<148, 384, smem>>>(streams, dc, sink, 12, getenv("NOWAIT") ? 1 : 0);
   cudaDeviceSynchronize();
   long long cyc;
   cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost);
+  printf("slots %d ", NSL);
   printf("convlike variant %d: %.1f cyc/MMA over %d MMAs (%s)\n", VARIANT, (double)cyc / (streams * 120), streams * 120,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(dc);
@@ -365,6 +367,8 @@ void run_convlike() {
 int main() {
   run_convlike<0>();
   run_convlike<8>();
+  run_convlike<8, 5>();
+  if (getenv("CONV_ONLY")) return 0;
   run_convlike<9>();
   run_convlike<7>();
   run_convlike<5>();

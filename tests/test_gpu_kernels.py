@@ -158,6 +158,36 @@ def test_tcgen05_and_mma_sync_kernels(oracle, K, bits):
                 assert res.mismatches == 0
 
 
+@pytest.mark.parametrize("off", [0, 1, 3])
+def test_tcgen05_output_windows(oracle, off):
+    """Output windows [y_begin, y_begin + n_out) at every 4-sample phase and
+    row bases at every 4-byte phase: the tcgen05 kernel shifts its tiles so
+    the input windows stay 16-byte aligned (the halo-split and host-pipeline
+    shapes), plain and fused."""
+    n, K = 30000, 256
+    p = nent.derive_params(3, 64)
+    c = rand(off + 40, (3, n), -2048, 2047)
+    g = rand(off + 41, (K,), -2048, 2047)
+    ref = oracle.full_conv(c, g)
+    big = torch.zeros((3, n + 8), dtype=torch.int32, device="cuda")
+    big[:, off:off + n] = torch.from_numpy(c).to(torch.int32)
+    x = big[:, off:off + n]
+    L = n + K - 1
+    fl_plain = imma_flavor(D.signed_digits(2048), D.signed_digits(2048))
+    fl = imma_flavor(D.signed_digits(2048 * ((1 << p.l) + 1)), D.signed_digits(2048))
+    assert D.imma_kernel(fl, K, 3, True) == "tcgen05"
+    gp, gf = D.taps_tensor(g, fl_plain), D.taps_tensor(g, fl)
+    for y0, cnt in [(0, L), (1, 9000), (2, 8193), (3, 1), (255, 20000), (4321, L - 4321), (L - 5, 5)]:
+        y, _ = D.conv(x, gp, K, fl_plain, period=L, y_begin=y0, n_out=cnt)
+        assert np.array_equal(y.cpu().numpy(), ref[:, y0:y0 + cnt]), ("plain", off, y0, cnt)
+        for r in (None, 2):
+            mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+            d = D.fused_conv(x, gf, K, p.l, fl, r, True, L, n_in=n, y_begin=y0, n_out=cnt,
+                             mismatch=mm if r is None else None)
+            assert np.array_equal(d.cpu().numpy(), ref[:, y0:y0 + cnt]), ("fused", off, y0, cnt, r)
+            assert int(mm.item()) == 0
+
+
 @pytest.mark.parametrize("off,pad", [(0, 0), (1, 0), (2, 5), (3, 1), (1, 3)])
 def test_imma_unaligned_rows(oracle, off, pad):
     """Row bases that are only 4-byte aligned (sliced buffers, halo-prefixed

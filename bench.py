@@ -476,14 +476,24 @@ def other_configs(D, fused, dev, stream):
         fl = fused.conv_flavor(xb, wl.g, n_out=L)
         gd = D.taps_tensor(wl.g, fl)
         tab = D.imma_table(gd, K, fl, 0)
+        # m > 3 chain: tcgen05 conv of the chain rows + verifying extract (the
+        # route fused.entangled_chain_conv takes), else the fused kernel
+        split = (chain and D.imma_kernel(fl, K, wl.m, True) != "tcgen05"
+                 and D.imma_kernel(fl, K, wl.m, False) == "tcgen05")
+        if split:
+            delta = torch.empty((wl.m, L), dtype=torch.int32, device=dev)
 
         def run():
             if chain:
                 from paper_1509_03838_b200._lib import call, ptr, row_ptrs, bits
                 call("nent_interleave", row_ptrs(c), 32, wl.m, n, ptr(ct), D._sh())
                 D.gather_chain(ct, p.l, wl.scale, add, perm, out=xg)
-                D.fused_conv(xg, gd, K, p.l, fl, None, True, L, n_in=n, out=out, mismatch=mm,
-                             pre_entangled=True, imma_table=tab)
+                if split:
+                    D.conv(xg, gd, K, fl, period=L, n_out=L, out=delta)
+                    D.extract_verify(delta, wl.m, p.l, 0, p.w > 32, mm, out=out)
+                else:
+                    D.fused_conv(xg, gd, K, p.l, fl, None, True, L, n_in=n, out=out, mismatch=mm,
+                                 pre_entangled=True, imma_table=tab)
             else:
                 D.fused_conv(c, gd, K, p.l, fl, None, True, L, n_in=n, out=out, mismatch=mm,
                              imma_table=tab)
@@ -496,7 +506,9 @@ def other_configs(D, fused, dev, stream):
         a, b = event_time(run, stream, reps)
         torch.cuda.synchronize(dev)
         ms = a.elapsed_time(b) / reps
-        res[f"cfg{cfg}"] = {"flavor": MAC_NAMES[fl], "ms": ms, "samples_per_s": wl.m * L / (ms / 1e3),
+        res[f"cfg{cfg}"] = {"flavor": MAC_NAMES[fl], "ms": ms,
+                            "kernel": (("tcgen05 conv + verifying extract" if split else D.imma_kernel(fl, K, wl.m, True))
+                                       if (fl & 0xFF) == 7 else "cuda-core"), "samples_per_s": wl.m * L / (ms / 1e3),
                             "conv_gmac_s": wl.m * n * K / (ms / 1e3) / 1e9, "exact": ok}
     # cfg4 inner products (65,536 x 4,096 per stream, 3 streams)
     wl = workloads.make(4)

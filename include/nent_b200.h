@@ -98,6 +98,15 @@ int nent_shift_add(const void *a, const void *b, int in_bits, void *out, int out
 int nent_extract(const void *const *delta, int delta_bits, void *const *out, int out_bits, int m,
                  int64_t n, int l, int r, int wide, unsigned long long *overflow_dev, void *stream);
 
+/* K3 with the redundant-stream check: recovers every row from the rows other
+ * than `pivot` (exactly nent_extract with r = pivot), then adds to
+ * *mismatch_dev the positions whose pivot word differs from the re-entangled
+ * recovery (d_{pivot-1} << l) + d_pivot -- the fused kernel's failed=None
+ * check as a separate pass (used after the plain tensor-core conv for m > 3). */
+int nent_extract_verify(const void *const *delta, int delta_bits, void *const *out, int out_bits, int m,
+                        int64_t n, int l, int pivot, int wide, unsigned long long *overflow_dev,
+                        unsigned long long *mismatch_dev, void *stream);
+
 /* Replaces codec.disentangle_m3 (codec.py:151-183), the independent m=3 recipe. */
 int nent_extract_m3(const void *const *delta, int delta_bits, void *const *out, int out_bits,
                     int64_t n, int l, int w, int r, void *stream);

@@ -173,6 +173,19 @@ def extract(delta, m: int, l: int, r: int, wide: bool, out_dtype=torch.int64,
     return out, (int(ovf.item()) if ovf is not None else 0)
 
 
+def extract_verify(delta: torch.Tensor, m: int, l: int, pivot: int, wide: bool, mismatch: torch.Tensor,
+                   out_dtype=torch.int64, out: torch.Tensor | None = None):
+    """K3 from the rows != pivot plus the redundant-stream check of row
+    `pivot`; mismatches are added to the device counter ``mismatch``."""
+    rows = [delta[i] for i in range(m)]
+    n = rows[0].shape[-1]
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype, device=delta.device)
+    call("nent_extract_verify", row_ptrs(rows), bits(delta), row_ptrs(out), bits(out), m, n, l, pivot,
+         int(bool(wide)), None, ptr(mismatch), _sh())
+    return out
+
+
 def extract_m3(delta: torch.Tensor, l: int, w: int, r: int, out_dtype=torch.int64):
     rows = [None if i == r else delta[i] for i in range(3)]
     out = torch.empty(delta.shape, dtype=out_dtype, device=delta.device)

@@ -14,58 +14,102 @@
 
 namespace nent {
 
-constexpr int TR_T = 32;
-
-// x rows (m x n) -> out (n x m), m <= 8: tile of 32 positions x m streams via smem
+// x rows (m x n) -> out (n x m), m <= 8: tiles of 4 KB per row x m streams
+// through shared memory; every thread issues all its row loads (16-byte
+// vectors for int32 rows) before the first store, so ~32 KB per SM are in
+// flight, and writes 16-byte vectors of the position-major output.
 template <typename T>
 __global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m, int64_t n, T* __restrict__ out) {
-  __shared__ T tile[8][TR_T * 8 + 1];
+  constexpr int P = 4096 / sizeof(T);        // positions per tile (1024 int32, 512 int64)
+  constexpr int V = 16 / sizeof(T);          // elements per 16-byte vector
+  __shared__ T tile[8][P + 16 / sizeof(T)];  // padded rows
   const int tid = threadIdx.x;
-  for (int64_t p0 = (int64_t)blockIdx.x * TR_T * 8; p0 < n; p0 += (int64_t)gridDim.x * TR_T * 8) {
-    // load: row s, positions p0 .. p0+255 (coalesced per row)
-    for (int i = tid; i < m * TR_T * 8; i += blockDim.x) {
-      const int s = i / (TR_T * 8), j = i % (TR_T * 8);
-      const int64_t p = p0 + j;
-      tile[s][j] = p < n ? reinterpret_cast<const T*>(x.p[s])[p] : (T)0;
+  for (int64_t p0 = (int64_t)blockIdx.x * P; p0 < n; p0 += (int64_t)gridDim.x * P) {
+    const bool full = p0 + P <= n;
+    bool vec = full;
+    for (int s = 0; s < m; ++s) vec = vec && ((reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(x.p[s]) + p0) & 15) == 0);
+    if (vec) {
+      // each thread: one vector of every row (P / V vectors per row = 256 threads for int32)
+      for (int i = tid; i < P / V; i += blockDim.x) {
+        int4 w[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < m) w[s] = __ldg(reinterpret_cast<const int4*>(reinterpret_cast<const T*>(x.p[s]) + p0) + i);
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < m) *reinterpret_cast<int4*>(&tile[s][V * i]) = w[s];
+      }
+    } else {
+      for (int i = tid; i < m * P; i += blockDim.x) {
+        const int s = i / P, j = i % P;
+        const int64_t p = p0 + j;
+        tile[s][j] = p < n ? reinterpret_cast<const T*>(x.p[s])[p] : (T)0;
+      }
     }
     __syncthreads();
-    // store: position-major, m consecutive values per position (coalesced)
-    for (int i = tid; i < m * TR_T * 8; i += blockDim.x) {
-      const int j = i / m, s = i % m;
-      const int64_t p = p0 + j;
-      if (p < n) out[p * m + s] = tile[s][j];
+    // position-major stores: element e = j*m + s of the tile's output span
+    const int64_t base = p0 * m;
+    const int64_t total = (full ? P : n - p0) * m;
+    if (full && m * sizeof(T) % 16 == 0 && (reinterpret_cast<uintptr_t>(out + base) & 15) == 0) {
+      for (int e = V * tid; e < total; e += V * blockDim.x) {
+        T v[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = tile[(e + k) % m][(e + k) / m];
+        *reinterpret_cast<int4*>(out + base + e) = *reinterpret_cast<const int4*>(v);
+      }
+    } else {
+      for (int e = tid; e < total; e += blockDim.x) out[base + e] = tile[e % m][e / m];
     }
     __syncthreads();
   }
 }
 
-// x_s[p] = scale * ((c_{s-1}[q] << l) + c_s[q]) + add[q],  q = perm[p]
+// x_s[p] = scale * ((c_{s-1}[q] << l) + c_s[q]) + add[q],  q = perm[p].
+// Each thread walks GU positions per round: all GU permutation indices first,
+// then all GU record and add gathers, so GU random sectors per thread are in
+// flight instead of one dependent pair.
+template <typename T, typename TO, int MT>
+__device__ __forceinline__ void gather_one(const T* __restrict__ ct, int64_t p, int64_t q, int l, int64_t scale,
+                                           int64_t a, MutRows& x) {
+  int64_t c[MT];
+  const T* row = ct + q * MT;
+  if (sizeof(T) == 4 && MT == 8) {
+    const int4 lo = __ldg(reinterpret_cast<const int4*>(row));
+    const int4 hi = __ldg(reinterpret_cast<const int4*>(row) + 1);
+    c[0] = lo.x; c[1] = lo.y; c[2] = lo.z; c[3] = lo.w;
+    c[4 % MT] = hi.x; c[5 % MT] = hi.y; c[6 % MT] = hi.z; c[7 % MT] = hi.w;
+  } else {
+#pragma unroll
+    for (int s = 0; s < MT; ++s) c[s] = (int64_t)__ldg(row + s);
+  }
+#pragma unroll
+  for (int s = 0; s < MT; ++s) {
+    int64_t e = wadd(wshl(c[(s + MT - 1) % MT], l), c[s]);
+    if (scale != 1) e = wmul(e, scale);
+    e = wadd(e, a);
+    reinterpret_cast<TO*>(x.p[s])[p] = (TO)(uint64_t)e;
+  }
+}
+
 template <typename T, typename TO, int MT>
 __global__ void __launch_bounds__(256)
 gather_chain_kernel(const T* __restrict__ ct, int64_t n, int l, int64_t scale, const void* add,
                     int add_bits, const int64_t* __restrict__ perm, MutRows x) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
+  constexpr int GU = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; p + (GU - 1) * stride < n; p += GU * stride) {
+    int64_t q[GU], a[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) q[u] = perm ? __ldg(perm + p + u * stride) : p + u * stride;
+#pragma unroll
+    for (int u = 0; u < GU; ++u) a[u] = add ? ld_bits(add, add_bits, q[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < GU; ++u) gather_one<T, TO, MT>(ct, p + u * stride, q[u], l, scale, a[u], x);
+  }
+  for (; p < n; p += stride) {
     const int64_t q = perm ? __ldg(perm + p) : p;
-    int64_t c[MT];
-    const T* row = ct + q * MT;
-    if (sizeof(T) == 4 && MT == 8) {
-      const int4 lo = __ldg(reinterpret_cast<const int4*>(row));
-      const int4 hi = __ldg(reinterpret_cast<const int4*>(row) + 1);
-      c[0] = lo.x; c[1] = lo.y; c[2] = lo.z; c[3] = lo.w;
-      c[4 % MT] = hi.x; c[5 % MT] = hi.y; c[6 % MT] = hi.z; c[7 % MT] = hi.w;
-    } else {
-#pragma unroll
-      for (int s = 0; s < MT; ++s) c[s] = (int64_t)__ldg(row + s);
-    }
-    const int64_t a = add ? ld_bits(add, add_bits, q) : 0;
-#pragma unroll
-    for (int s = 0; s < MT; ++s) {
-      int64_t e = wadd(wshl(c[(s + MT - 1) % MT], l), c[s]);
-      if (scale != 1) e = wmul(e, scale);
-      e = wadd(e, a);
-      reinterpret_cast<TO*>(x.p[s])[p] = (TO)(uint64_t)e;
-    }
+    gather_one<T, TO, MT>(ct, p, q, l, scale, add ? ld_bits(add, add_bits, q) : 0, x);
   }
 }
 
@@ -80,7 +124,7 @@ int nent_interleave(const void* const* x, int x_bits, int m, int64_t n, void* ou
   if (m < 1 || m > 8 || n < 0) { set_error("interleave: m=%d not in 1..8", m); return NENT_ERR_PARAM; }
   if (n == 0) return NENT_OK;
   Rows R = to_rows(x, m);
-  const int grid = grid_for(n, TR_T * 8, 1, 148 * 16);
+  const int grid = grid_for(n, x_bits == 32 ? 1024 : 512, 1, 148 * 8);
   cudaStream_t s = as_stream(stream);
   if (x_bits == 32) interleave_kernel<int32_t><<<grid, 256, 0, s>>>(R, m, n, (int32_t*)out);
   else interleave_kernel<int64_t><<<grid, 256, 0, s>>>(R, m, n, (int64_t*)out);

@@ -75,7 +75,7 @@ shift_add_kernel(const TI* __restrict__ a, const TI* __restrict__ b, TO* __restr
 template <int MT, typename TI, typename TO>
 __global__ void __launch_bounds__(EW_THREADS)
 extract_kernel(const Rows delta, MutRows out, int m, int64_t n, int l, int r, int wide,
-               unsigned long long* overflow) {
+               unsigned long long* overflow, unsigned long long* mismatch) {
   constexpr int CAP = MT > 0 ? MT : NENT_MAX_STREAMS;
   const int M = MT > 0 ? MT : m;
   for (int64_t j = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; j < n;
@@ -95,6 +95,13 @@ extract_kernel(const Rows delta, MutRows out, int m, int64_t n, int l, int r, in
       int row = r + t;
       row -= row >= M ? M : 0;
       reinterpret_cast<TO*>(out.p[row])[j] = (TO)(uint64_t)orot[t];
+    }
+    // verify: the pivot's own word must be (d_{r-1} << l) + d_r (codec.py:57-66)
+    if (mismatch) {
+      const int64_t dr = (int64_t)__ldg(reinterpret_cast<const TI*>(delta.p[r]) + j);
+      int64_t want = wadd(wshl(orot[M - 1], l), orot[0]);
+      if (sizeof(TI) == 4) want = (int64_t)(int32_t)(uint32_t)(uint64_t)want;  // the row's own width
+      if (dr != want) atomicAdd(mismatch, 1ull);
     }
   }
 }
@@ -257,9 +264,9 @@ int nent_shift_add(const void* a, const void* b, int in_bits, void* out, int out
   return check_launch("shift_add");
 }
 
-int nent_extract(const void* const* delta, int delta_bits, void* const* out, int out_bits, int m,
-                 int64_t n, int l, int r, int wide, unsigned long long* overflow_dev,
-                 void* stream) {
+static int extract_impl(const void* const* delta, int delta_bits, void* const* out, int out_bits, int m,
+                        int64_t n, int l, int r, int wide, unsigned long long* overflow_dev,
+                        unsigned long long* mismatch_dev, void* stream) {
   NENT_CHECK_BITS(delta_bits);
   NENT_CHECK_BITS(out_bits);
   if (m < 3 || m > NENT_MAX_STREAMS || r < 0 || r >= m || l < 1 || (m - 1) * l > 63) {
@@ -269,13 +276,17 @@ int nent_extract(const void* const* delta, int delta_bits, void* const* out, int
   if (n <= 0) return NENT_OK;
   cudaStream_t s = as_stream(stream);
   Rows D = to_rows(delta, m);
-  D.p[r] = nullptr;  // the failed stream is never dereferenced
+  if (!mismatch_dev) D.p[r] = nullptr;  // the failed stream is never dereferenced
+  else if (!D.p[r]) {
+    set_error("extract_verify: the pivot row %d must be given", r);
+    return NENT_ERR_PARAM;
+  }
   MutRows O = to_mrows(out, m);
   int grid = grid_for(n, EW_THREADS, 4);
 #define EXTRACT_CASE(MTV)                                                                  \
   DISPATCH_IO(delta_bits, out_bits,                                                        \
               (extract_kernel<MTV, TI, TO><<<grid, EW_THREADS, 0, s>>>(D, O, m, n, l, r, wide, \
-                                                                      overflow_dev)))
+                                                                      overflow_dev, mismatch_dev)))
   switch (m) {
     case 3: EXTRACT_CASE(3); break;
     case 4: EXTRACT_CASE(4); break;
@@ -285,6 +296,22 @@ int nent_extract(const void* const* delta, int delta_bits, void* const* out, int
   }
 #undef EXTRACT_CASE
   return check_launch("extract");
+}
+
+int nent_extract(const void* const* delta, int delta_bits, void* const* out, int out_bits, int m,
+                 int64_t n, int l, int r, int wide, unsigned long long* overflow_dev, void* stream) {
+  return extract_impl(delta, delta_bits, out, out_bits, m, n, l, r, wide, overflow_dev, nullptr, stream);
+}
+
+int nent_extract_verify(const void* const* delta, int delta_bits, void* const* out, int out_bits, int m,
+                        int64_t n, int l, int pivot, int wide, unsigned long long* overflow_dev,
+                        unsigned long long* mismatch_dev, void* stream) {
+  if (!mismatch_dev) {
+    set_error("extract_verify: mismatch counter required");
+    return NENT_ERR_PARAM;
+  }
+  return extract_impl(delta, delta_bits, out, out_bits, m, n, l, pivot, wide, overflow_dev, mismatch_dev,
+                      stream);
 }
 
 int nent_extract_m3(const void* const* delta, int delta_bits, void* const* out, int out_bits,

@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._lib import MAC_G64, MAC_NAMES, MAC_W64, MAC_X128
+from ._lib import MAC_G64, MAC_NAMES, MAC_W64, MAC_X128, is_imma
 from .blocks import StreamBlock
 from .errors import DeviceError, ParameterError
 from .params import CodecParams
@@ -147,10 +147,26 @@ def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: i
     if flavor is None:
         flavor = conv_flavor(x_bound, g, n_out=n + K - 1, gather=not two_pass)
     g_dev = D.taps_tensor(g, flavor)
+    L = n + K - 1
     if two_pass:
         x = D.gather_chain(D.interleave(c), p.l, scale, add_ent, perm_dev, out_dtype=torch.int32)
-        d = D.fused_conv(x, g_dev, K, p.l, flavor, failed, p.w > 32, n + K - 1, n_in=n,
-                         out_dtype=out_dtype, mismatch=mismatch, pre_entangled=True)
+        if (is_imma(flavor) and D.imma_kernel(flavor, K, m, True) != "tcgen05"
+                and D.imma_kernel(flavor, K, m, False) == "tcgen05"):
+            # m > 3: the fused tensor-core kernel would be the mma.sync one; the
+            # tcgen05 kernel convolves the m chain rows (the workers' entangled
+            # outputs) and a separate pass recovers them (+ the redundant check)
+            wide_delta = x_bound * int(np.abs(g.astype(object)).sum()) >= 1 << 31
+            delta, _ = D.conv(x, g_dev, K, flavor, period=L, n_out=L,
+                              out_dtype=torch.int64 if wide_delta else torch.int32)
+            if failed is None:
+                d = D.extract_verify(delta, m, p.l, 0, p.w > 32, mismatch if mismatch is not None
+                                     else torch.zeros(1, dtype=torch.int64, device=c.device),
+                                     out_dtype=out_dtype)
+            else:
+                d, _ = D.extract(delta, m, p.l, failed, p.w > 32, out_dtype=out_dtype)
+        else:
+            d = D.fused_conv(x, g_dev, K, p.l, flavor, failed, p.w > 32, L, n_in=n,
+                             out_dtype=out_dtype, mismatch=mismatch, pre_entangled=True)
     else:
         d = D.fused_conv(c, g_dev, K, p.l, flavor, failed, p.w > 32, n + K - 1, n_in=n,
                          scale=scale, add=add_ent, perm=perm_dev, out_dtype=out_dtype,

@@ -278,6 +278,42 @@ def test_chain_conv_cfg5_shape(oracle):
             assert res.mismatches == 0
 
 
+@pytest.mark.parametrize("mma_sync", [False, True])
+def test_chain_conv_cfg5_tensor_core_routes(oracle, mma_sync):
+    """cfg5's chain on the tensor cores: the fused mma.sync kernel, or (m = 8 is
+    outside the fused tcgen05 envelope) the tcgen05 conv of the chain rows
+    followed by the verifying extract pass -- same outputs, same check."""
+    from paper_1509_03838_b200 import workloads
+    wl = workloads.make(5, n=3 * 8192 + 500)
+    x = (wl.c * wl.scale + wl.add)[:, wl.perm]
+    ref = oracle.full_conv(x, wl.g)
+    fl = imma_flavor(2, 1, mma_sync)
+    assert D.imma_kernel(fl, wl.K, 8, False) == ("mma.sync" if mma_sync else "tcgen05")
+    for r in [None, 0, 5]:
+        res = fused.entangled_chain_conv(nent.StreamBlock(wl.params, wl.c), wl.scale, wl.add,
+                                         wl.perm, wl.g, failed=r, flavor=fl)
+        assert np.array_equal(res.outputs.data, ref), (mma_sync, r)
+        if r is None:
+            assert res.mismatches == 0
+
+
+def test_extract_verify_counts_inconsistent_words(oracle):
+    """nent_extract_verify flags exactly the positions whose pivot word is not
+    the re-entangled recovery."""
+    p = nent.derive_params(5, 32)
+    c = rand(77, (5, 4000), -100, 100)
+    eps = oracle.entangle(c, p.l)
+    delta = torch.from_numpy(eps).cuda()
+    mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+    d = D.extract_verify(delta, 5, p.l, 0, False, mm)
+    assert np.array_equal(d.cpu().numpy(), c) and int(mm.item()) == 0
+    delta[0, 17] += 1
+    delta[0, 3999] -= 5
+    mm.zero_()
+    D.extract_verify(delta, 5, p.l, 0, False, mm)
+    assert int(mm.item()) == 2
+
+
 def test_chain_conv_single_stream_worker(oracle):
     """The stream-per-GPU worker: one entangled stream (a << l) + b, chain, conv."""
     from paper_1509_03838_b200 import workloads

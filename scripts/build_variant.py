@@ -1,0 +1,28 @@
+"""Build a profiling variant of libnent_b200.so into scripts/_bin/ with extra
+nvcc defines, e.g. `python scripts/build_variant.py timers -DNENT_TC05_TIMERS`."""
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1509_03838_b200 import _build as B  # noqa: E402
+
+name, defs = sys.argv[1], sys.argv[2:]
+out = Path(__file__).resolve().parent / "_bin"
+obj = out / f"obj_{name}"
+obj.mkdir(parents=True, exist_ok=True)
+nvcc = B._nvcc()
+
+
+def one(src):
+    o = obj / (src.stem + ".o")
+    subprocess.run([nvcc, *B.NVCC_FLAGS, *defs, "-c", str(src), "-o", str(o)], check=True)
+    return o
+
+
+with ThreadPoolExecutor(8) as ex:
+    objs = list(ex.map(one, sorted(B.CSRC.glob("*.cu"))))
+subprocess.run([nvcc, *B.ARCH, "-shared", "-cudart", "static", "-o", str(out / f"libnent_b200_{name}.so"),
+                *map(str, objs), "-lrt", "-ldl", "-lpthread"], check=True)
+print(out / f"libnent_b200_{name}.so")

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+timeout 300 python scripts/tc05_debug.py 0 1 2 3 4 6 5 7 > gpurun_out/tc05_debug.log 2>&1
+timeout 300 python scripts/tc05_timers.py 0 1 2 4 > gpurun_out/tc05_timers.log 2>&1
+timeout 300 python scripts/tc05_one.py > gpurun_out/plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:conv_tc05 -s 1 -c 1 \
+    -o gpurun_out/prof_tc05 python scripts/tc05_one.py > gpurun_out/ncu.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu.log

@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     const int RL = G.KT + 128;
     unsigned char* rev = smem_raw + (stage_s - tc05::smem_u32(smem_raw));
     const uint64_t gbias = bias_of(NG);
-    for (int i = tid; i < RL; i += NT) {
+    for (int i = tid; i < ((G.debug & 32768) ? 0 : RL); i += NT) {
       const int idx = G.KT - 1 - i;
       const int64_t gv = (idx >= 0 && idx < A.K) ? ld_bits(A.g, A.g_bits, idx) : 0;
       const uint64_t d = digits_of(gv, gbias);
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     // lane v of quadrant warp&3 holds row v of A_j; 32-byte K steps are spread
     // over the three warps of each quadrant
     const int v = 32 * (warp & 3) + lane;
-    for (int blk = warp >> 2; blk < NG * G.nsteps; blk += NT / 128) {
+    for (int blk = warp >> 2; blk < ((G.debug & 32768) ? 0 : NG * G.nsteps); blk += NT / 128) {
       const int j = blk / G.nsteps, kc = blk % G.nsteps;
       const unsigned char* r = rev + j * RL + 32 * kc - v + 127;
       uint32_t w[8];
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
         for (int q = 0; q < G.nstreams; ++q, ++seq, cls += NCLS) {
           const int slot = seq & 1;
           if (!(G.debug & 1024)) TC05_TIMED(0, mb_wait(full_b(slot), (uint32_t)((seq >> 1) & 1)));
-          tc05::fence_after();
+          if (!(G.debug & 2048)) tc05::fence_after();
           for (int p = 0; p < NP; ++p) {
             const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * NP + p) * PLANE));
             for (int j = 0; j < NG; ++j) {
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
               if (p == (c < NP - 1 ? c : NP - 1)) tc05::commit_elect(accf_b(rs));
             }
           }
-          tc05::commit_elect(empty_b(slot));
+          if (!(G.debug & 4096)) tc05::commit_elect(empty_b(slot));
         }
       }
     }
@@ -500,11 +500,11 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     PUnit cur = first_unit();
     PUnit nxt = next_unit(cur);
     issue(0, cur);
-    for (int64_t H = 0; H < units; ++H, cur = nxt, nxt = next_unit(nxt)) {
+    for (int64_t H = (G.debug & 16384) ? units : 0; H < units; ++H, cur = nxt, nxt = next_unit(nxt)) {
       const int64_t seq = H >> 1;
       const int slot = (int)(seq & 1);
       const int h = cur.h, row = cur.row;
-      if (h == 0 && seq >= 2) TC05_TIMED(0, mb_wait_sleep(empty_b(slot), (uint32_t)(((seq >> 1) - 1) & 1)));
+      if (h == 0 && seq >= 2 && !(G.debug & 4096)) TC05_TIMED(0, mb_wait_sleep(empty_b(slot), (uint32_t)(((seq >> 1) - 1) & 1)));
       issue(H + 1, nxt);
       if (cur.mode == 1 && !(G.debug & 32)) {
         const int sb = (int)(H & 1);
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     const uint64_t corr = 0 - 128 * gsum * ones;
     unsigned bad = 0;
     int64_t cls = 0;
-    for (int64_t tile = blockIdx.x; tile < G.ntiles; tile += gridDim.x) {
+    for (int64_t tile = (G.debug & 8192) ? G.ntiles : blockIdx.x; tile < G.ntiles; tile += gridDim.x) {
       const int64_t ybase = tile * TILE - G.shift;  // output index of (u=0, v=0)
       // every output of the tile inside [0, n_out) and int32 rows: unconditional
       // stores at immediate offsets from one per-thread base pointer

@@ -114,7 +114,7 @@ probe(const int8_t* A, const int8_t* B, int N, int row0, int reps, int mode, int
 
 // throughput only: NACC accumulators x 12 K steps, fully unrolled, descriptors hoisted
 template <int N, int MODE, int NACC, bool SAMEB, int CE>
-__global__ void __launch_bounds__(128, 1) tput(int reps, long long* cycles) {
+__global__ void __launch_bounds__(128, 1) tput(int reps, long long* cycles, int doff) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t mbar, mbar2;
@@ -145,9 +145,9 @@ __global__ void __launch_bounds__(128, 1) tput(int reps, long long* cycles) {
 #pragma unroll
         for (int a = 0; a < NACC; ++a) {
           if (MODE == 0)
-            tc05::mma_i8_ts(tbase + 128 + a * N, tbase + 8 * kc, bd[kc], idesc, 1);
+            tc05::mma_i8_ts(tbase + doff + a * N, tbase + 8 * kc, bd[kc], idesc, 1);
           else
-            tc05::mma_i8_ss(tbase + 128 + a * N, ad[kc], bd[kc], idesc, 1);
+            tc05::mma_i8_ss(tbase + doff + a * N, ad[kc], bd[kc], idesc, 1);
           if (CE && (kc + 1) % (CE ? CE : 1) == 0) tc05::commit(tc05::smem_u32(&mbar2));
         }
     tc05::commit(tc05::smem_u32(&mbar));
@@ -166,12 +166,12 @@ void run_tput(int grid = 1) {
   const int smem = 3 * 16384 + 128 * (N + 4) + 1024;
   cudaFuncSetAttribute(tput<N, MODE, NACC, SAMEB, CE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int reps = 2000;
-  tput<N, MODE, NACC, SAMEB, CE><<<grid, 128, smem>>>(reps, dc);
+  tput<N, MODE, NACC, SAMEB, CE><<<grid, 128, smem>>>(reps, dc, getenv("DOFF") ? atoi(getenv("DOFF")) : 128);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  tput<N, MODE, NACC, SAMEB, CE><<<grid, 128, smem>>>(reps, dc);
+  tput<N, MODE, NACC, SAMEB, CE><<<grid, 128, smem>>>(reps, dc, getenv("DOFF") ? atoi(getenv("DOFF")) : 128);
   cudaEventRecord(e1);
   cudaDeviceSynchronize();
   float ms = 0;
@@ -192,7 +192,7 @@ void run_tput(int grid = 1) {
 // 3: + 8 warps streaming tcgen05.ld of the accumulator ring; 4: + 8 warps of
 // STS traffic to shared memory
 template <int VARIANT, int NSL = 3>
-__global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycles, unsigned long long* sink, int nsteps_rt, int getenv_nowait) {
+__global__ void __launch_bounds__(512, 1) convlike(int streams, long long* cycles, unsigned long long* sink, int nsteps_rt, int getenv_nowait) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t mbar, mbar2, accf[5], acce[5];
@@ -229,7 +229,49 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
   tc05::fence_before();
   __syncthreads();
   tc05::fence_after();
-  if (warp == 0) {
+  if (VARIANT == 10) {  // the conv kernel's register split
+    if (warp >= 4 && warp < 12) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+  }
+  if (VARIANT == 11 && warp == 0) {  // the conv kernel's MMA loop, verbatim structure
+    constexpr int NP = 5, NG = 2, NCLS = 6, NSTEPS = 12, SLOTS = NSL, U = 64, PLANE = 9216;
+    const uint32_t idesc = tc05::idesc_i8(128, U, false);
+    const uint32_t planes_s = tc05::smem_u32(smem);
+    const uint32_t tbase = 0, RING0 = 512 - 64 * NSL;
+    const bool skip = nsteps_rt == 99;
+    const long long t0 = clock64();
+    int seq = 0, cls = 0;
+    const int64_t ntiles = 2049;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int q = 0; q < 3; ++q, ++seq, cls += NCLS) {
+        const int slot = seq & 1;
+        for (int p = 0; p < NP; ++p) {
+          const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * NP + p) * PLANE));
+          for (int j = 0; j < NG; ++j) {
+            const int c = p + j;
+            const int k = cls + c;
+            const int rs = k % SLOTS;
+            const bool first = p == (c - NG + 1 > 0 ? c - NG + 1 : 0);
+            const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
+            const uint32_t a = tbase + (uint32_t)(8 * j * NSTEPS);
+            if (!skip && elect_one_probe()) {
+#pragma unroll
+              for (int kc = 0; kc < NSTEPS; ++kc)
+                tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
+            }
+            __syncwarp();
+            if (p == (c < NP - 1 ? c : NP - 1)) tc05::commit_elect(tc05::smem_u32(&mbar2));
+          }
+        }
+      }
+    }
+    tc05::commit_elect(tc05::smem_u32(&mbar));
+    mbar_wait(tc05::smem_u32(&mbar), 0);
+    if (threadIdx.x == 0) {
+      *cycles = (clock64() - t0) * 5040 / (seq * 120);
+      stop_flag = 1;
+    }
+  } else if (warp == 0) {
     const uint32_t idesc = tc05::idesc_i8(128, 64, false);
     const uint32_t planes_s = tc05::smem_u32(smem);
     const long long t0 = clock64();
@@ -245,7 +287,7 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
             mbar_wait(tc05::smem_u32(&acce[rs]), (use - 1) & 1);
             tc05::fence_after();
           }
-          const uint32_t d = (NSL == 5 ? 192u : 320u) + 64u * rs, a = 96u * j;
+          const uint32_t d = (uint32_t)(512 - 64 * NSL) + 64u * rs, a = 96u * j;
           if (VARIANT == 6) {  // runtime step count in chunks of 4 (KT padded to 128)
             if (elect_one_probe()) {
               for (int k0 = 0; k0 < nsteps_rt; k0 += 4) {
@@ -263,7 +305,7 @@ __global__ void __launch_bounds__(384, 1) convlike(int streams, long long* cycle
                   tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
             }
             __syncwarp();
-          } else if (VARIANT == 0 || VARIANT == 7 || VARIANT == 8 || VARIANT == 9) {
+          } else if (VARIANT == 0 || VARIANT == 7 || VARIANT == 8 || VARIANT == 9 || VARIANT == 10) {
             if (elect_one_probe()) {
 #pragma unroll
               for (int kc = 0; kc < 12; ++kc) tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
@@ -349,12 +391,12 @@ template <int VARIANT, int NSL = 3>
 void run_convlike() {
   long long* dc;
   cudaMalloc(&dc, 8);
-  const int smem = 2 * 5 * 9216 + 8192;
+  const int smem = getenv("BIGSMEM") ? 229376 : 2 * 5 * 9216 + 8192;
   cudaFuncSetAttribute(convlike<VARIANT, NSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int streams = 42;
   unsigned long long* sink;
   cudaMalloc(&sink, (size_t)8 * (512 + 148 * 32768));
-  convlike<VARIANT, NSL><<<148, 384, smem>>>(streams, dc, sink, 12, getenv("NOWAIT") ? 1 : 0);
+  convlike<VARIANT, NSL><<<148, getenv("T512") ? 512 : 384, smem>>>(streams, dc, sink, 12, getenv("NOWAIT") ? 1 : 0);
   cudaDeviceSynchronize();
   long long cyc;
   cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost);
@@ -365,6 +407,19 @@ void run_convlike() {
 }
 
 int main() {
+  if (getenv("SMR")) {
+    run_convlike<0>();
+    run_convlike<11, 5>();
+    run_convlike<11, 3>();
+    return 0;
+  }
+  if (getenv("TPUT_FIRST")) {
+    run_tput<64, 0, 1, false>(148);
+    run_tput<64, 0, 2, false>(148);
+    run_tput<64, 0, 1, true>(148);
+    run_tput<128, 0, 1, false>(148);
+    return 0;
+  }
   run_convlike<0>();
   run_convlike<8>();
   run_convlike<8, 5>();

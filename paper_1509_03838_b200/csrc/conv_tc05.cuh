@@ -383,8 +383,13 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           const int slot = seq & 1;
           if (!(G.debug & 1024)) TC05_TIMED(0, mb_wait(full_b(slot), (uint32_t)((seq >> 1) & 1)));
           if (!(G.debug & 2048)) tc05::fence_after();
+          // fully unrolled: every TMEM / descriptor operand of the chain is then an
+          // immediate or a hoisted uniform register (a runtime (p, j) loop rebuilds
+          // them with R2UR moves between chains and costs ~30% of the MMA rate)
+#pragma unroll
           for (int p = 0; p < NP; ++p) {
             const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * NP + p) * PLANE));
+#pragma unroll
             for (int j = 0; j < NG; ++j) {
               const int c = p + j;
               const int k = cls + c;

@@ -147,7 +147,9 @@ int nent_imma_table(const void *g, int g_bits, int K, int64_t y_begin, int flavo
  * checked against the recovered outputs (silent-error detection) and the
  * number of inconsistent positions is added to *mismatch_dev.
  * pre_entangled != 0: the rows c are already entangled words (e.g. produced
- * by the stream-per-GPU workers or a gather pre-pass); only conv + extract. */
+ * by the stream-per-GPU workers or a gather pre-pass); only conv + extract.
+ * d_bits = 32 is for outputs whose admitted bound fits int32 (the reference's
+ * admit(), ops.py:127); outside that bound int32 results are unspecified. */
 int nent_fused_conv(const void *const *c, int c_bits, int m, int64_t n_in, int64_t period,
                     int l, int64_t scale, const void *add, int add_bits, const int64_t *perm,
                     const void *g, int g_bits, int K, int r, int pre_entangled, void *const *d,

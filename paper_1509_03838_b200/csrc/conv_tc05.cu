@@ -71,6 +71,8 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
   Geom G;
   size_t smem = 0;
   if (!tc05_geometry(A.K, A.rows, np, ng, extract, G, smem)) return NENT_TC05_NA;
+  for (int r = 0; r < A.rows; ++r)  // the producers' 32-bit entangling shift needs l in [1, 31]
+    if (A.a.p[r] && (A.l < 1 || A.l > 31)) return NENT_TC05_NA;
   { const char* e = getenv("NENT_TC05_DEBUG"); G.debug = e ? atoi(e) : 0; }
   const int sms = sm_count_tc();
   if (sms <= 0) return NENT_TC05_NA;

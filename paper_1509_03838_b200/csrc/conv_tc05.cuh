@@ -258,11 +258,16 @@ __device__ __forceinline__ void fill_half(uint32_t st, uint32_t pl, uint32_t w0,
     uint64_t u[4] = {(uint64_t)(int64_t)bv.x + bias, (uint64_t)(int64_t)bv.y + bias, (uint64_t)(int64_t)bv.z + bias,
                      (uint64_t)(int64_t)bv.w + bias};
     if (ENT) {
+      // + (a << l) as a {lo, hi} pair: the high word is a >> (32 - l) directly
+      // (l in [1, 31], checked on the host), so each position costs one shift
+      // pair and one 64-bit add
       const int4 av = lds128(st + HALFB + (uint32_t)(i * PT) * 16u);
-      u[0] += (uint64_t)(int64_t)av.x << l;
-      u[1] += (uint64_t)(int64_t)av.y << l;
-      u[2] += (uint64_t)(int64_t)av.z << l;
-      u[3] += (uint64_t)(int64_t)av.w << l;
+      const int av4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t sh = ((uint64_t)(uint32_t)(av4[e] >> (32 - l)) << 32) | (uint32_t)((uint32_t)av4[e] << l);
+        u[e] += sh;
+      }
     }
     put4<NP>(pl + tc05::sw128(4u * (w0 + (uint32_t)(PT * i))), u);
   }
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
       const int64_t ybase = tile * TILE - G.shift;  // output index of (u=0, v=0)
       // every output of the tile inside [0, n_out) and int32 rows: unconditional
       // stores at immediate offsets from one per-thread base pointer
-      const bool fast = A.y_bits == 32 && ybase >= 0 && ybase + TILE <= A.n_out;
+      const bool fast = A.y_bits == 32 && A.l < 32 && ybase >= 0 && ybase + TILE <= A.n_out;
       const int64_t o0 = ybase + 128 * (32 * half) + v;  // this thread's first output
       for (int q = 0; q < G.nstreams; ++q, cls += NCLS) {
         uint64_t acc[32];
@@ -647,24 +652,26 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           void* y1 = A.y.p[pivot + 1 >= 3 ? pivot - 2 : pivot + 1];
           void* y2 = A.y.p[pivot + 2 >= 3 ? pivot - 1 : pivot + 2];
           if (fast) {
-            // M = 3 recovery (recover_rot_valid<3>) on consistent words:
-            // t = (delta_{P+1} << l) - delta_{P+2}, v = sext_{2l}(t),
-            // d_{P+2} = -v, d_{P+1} = (delta_{P+2} + v) >> l, d_P = (delta_{P+1} - d_{P+1}) >> l
+            // M = 3 recovery (recover_rot_valid<3>) on consistent words whose
+            // recovered outputs fit int32 (the y_bits == 32 contract):
+            // v = sext_{2l}((delta_{P+1} << l) - delta_{P+2}) = -d_{P+2} is an
+            // int32, so its low word alone gives it; then
+            // d_{P+1} = (delta_{P+2} + v) >> l and d_P = (delta_{P+1} - d_{P+1}) >> l
             int32_t* z0 = reinterpret_cast<int32_t*>(y0) + o0;
             int32_t* z1 = reinterpret_cast<int32_t*>(y1) + o0;
             int32_t* z2 = reinterpret_cast<int32_t*>(y2) + o0;
-            const int l = A.l, sh = 64 - 2 * A.l;
+            const int l = A.l;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const uint64_t da = lds64(stash + SSTEP * i), db = acc[i];
-              const int64_t vv = (int64_t)(((da << l) - db) << sh) >> sh;
-              const int64_t d1 = (int64_t)(db + (uint64_t)vv) >> l;
-              const int64_t d0 = (int64_t)(da - (uint64_t)d1) >> l;
-              z0[128 * i] = (int32_t)d0;
-              z1[128 * i] = (int32_t)d1;
+              const int32_t vv = (int32_t)(((uint32_t)da << l) - (uint32_t)db);
+              const int32_t d1 = (int32_t)((int64_t)(db + (uint64_t)(int64_t)vv) >> l);
+              const int32_t d0 = (int32_t)((int64_t)(da - (uint64_t)(int64_t)d1) >> l);
+              z0[128 * i] = d0;
+              z1[128 * i] = d1;
               z2[128 * i] = (int32_t)(0u - (uint32_t)vv);
               // the pivot stream's word must equal (d_{P+2} << l) + d_P
-              if (A.r < 0) sts64(stash + SSTEP * i, (uint64_t)d0 - ((uint64_t)vv << l));
+              if (A.r < 0) sts64(stash + SSTEP * i, (uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << l));
             }
           } else {
 #pragma unroll

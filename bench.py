@@ -225,6 +225,10 @@ def run_ours(args):
                      y_begin=y_begin, n_out=n_out, out=d_dev, mismatch=mismatch,
                      imma_table=tables[fl])
 
+    def failed_step(r=1, fl=flavor):  # one stream lost: recovery from the two survivors
+        D.fused_conv(x_dev, taps[fl], K, params.l, fl, r, params.w > 32, period, n_in=n_in,
+                     y_begin=y_begin, n_out=n_out, out=d_dev, imma_table=tables[fl])
+
     def plain(fl):
         D.conv(x_dev, taps[fl], K, fl, period=period, y_begin=y_begin, n_out=n_out, out=y_plain,
                imma_table=tables[fl])
@@ -263,6 +267,7 @@ def run_ours(args):
     cands = {
         "entangled": lambda: fused_step(flavor),
         "entangled_cuda_core": lambda: fused_step(core_flavor),
+        "entangled_failed_r1": lambda: failed_step(1),
         "plain_same_kernel": lambda: plain(plain_same),
         "plain_fastest": lambda: plain(plain_fast),
         "plain_cuda_core_same_width": lambda: plain(core_flavor),
@@ -372,7 +377,9 @@ def run_ours(args):
                 "ms": med,
                 "note": "plain_same_kernel runs the identical kernel/digit geometry on the plain streams "
                         "(isolates entangle+extract); plain_fastest uses the digits the 12-bit plain "
-                        "samples need (2 planes instead of the entangled words' 5)"},
+                        "samples need (2 planes instead of the entangled words' 5); entangled_failed_r1 "
+                        "loses stream 1: the two survivors are convolved and all three outputs recovered "
+                        "(the lost stream is never computed)"},
             "roofline": {"bound": "tensor",
                          "pipe": ("tcgen05.mma kind::i8 (5th-gen tensor cores, TMEM accumulators)"
                                   if kernel_kind == "tcgen05" else "IMMA (mma.sync m16n8k32 s8)"),

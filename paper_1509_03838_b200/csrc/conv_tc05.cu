@@ -73,6 +73,9 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
   if (!tc05_geometry(A.K, A.rows, np, ng, extract, G, smem)) return NENT_TC05_NA;
   for (int r = 0; r < A.rows; ++r)  // the producers' 32-bit entangling shift needs l in [1, 31]
     if (A.a.p[r] && (A.l < 1 || A.l > 31)) return NENT_TC05_NA;
+  // fused with a failed stream: only the two survivors are convolved (the
+  // failed stream's delta is never produced, as in the reference's recovery)
+  if (extract && A.r >= 0) G.nstreams = 2;
   { const char* e = getenv("NENT_TC05_DEBUG"); G.debug = e ? atoi(e) : 0; }
   const int sms = sm_count_tc();
   if (sms <= 0) return NENT_TC05_NA;

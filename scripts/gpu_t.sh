@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python scripts/tc05_timers.py 0 256 1 128 32 160 > gpurun_out/t_timers.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x -p no:cacheprovider > gpurun_out/q_tests.log 2>&1; echo "rc=$?" >> gpurun_out/q_tests.log
+timeout 600 python bench.py --steps 50 --warmup 3 --no-cpu-baseline > gpurun_out/q_bench.log 2>&1; echo "rc=$?" >> gpurun_out/q_bench.log

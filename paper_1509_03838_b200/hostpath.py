@@ -125,38 +125,56 @@ class ChunkedEntangledConv:
         if h1 > h0:
             D.copy_rows(d_host[:, h0:h1], yb[:, h0 - ys:h1 - ys])
 
-    def run(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None) -> int:
-        """Enqueue the whole job; returns the number of kernels launched.
-        Call ``synchronize()`` before reading ``d_host``."""
+    def _check_host(self, c_host: torch.Tensor, d_host: torch.Tensor):
+        m, n, L = self.p.m, self.n, self.L
         if not c_host.is_pinned() or not d_host.is_pinned():
             raise ParameterError("host buffers must be pinned (torch.empty(..., pin_memory=True))")
-        m, H, n, L = self.p.m, self.HP, self.n, self.L
         if tuple(c_host.shape) != (m, n) or tuple(d_host.shape) != (m, L):
             raise ParameterError(f"expected c_host {(m, n)} and d_host {(m, L)}")
         if c_host.stride(1) != 1 or d_host.stride(1) != 1:
             raise ParameterError("host rows must be contiguous")
-        nch = len(self.bounds)
+
+    def run(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None) -> int:
+        """Enqueue the whole job; returns the number of kernels launched.
+        Call ``synchronize()`` before reading ``d_host``."""
+        return self.run_many([(c_host, d_host)], failed)
+
+    def run_many(self, jobs, failed: int | None = None) -> int:
+        """Enqueue several jobs ((c_host, d_host) pairs) as one continuous
+        chunk pipeline: the next job's first input copies overlap the previous
+        job's last kernels and output copies, so the pipeline fills and drains
+        once for the whole batch of jobs instead of once per job."""
+        for c_host, d_host in jobs:
+            self._check_host(c_host, d_host)
+        n, H = self.n, self.HP
+        seq = [(jb, s, e) for jb in range(len(jobs)) for (s, e) in self.bounds]
+        nch = len(seq)
         in_ev = [torch.cuda.Event() for _ in range(nch)]
         comp_ev = [torch.cuda.Event() for _ in range(nch)]
         out_ev = [torch.cuda.Event() for _ in range(nch)]
         # output copy starts: row 0's aligned word at or below each chunk boundary
-        hs = [0] + [max(s - self._lead(d_host, 0, s), 0) for s, _ in self.bounds[1:]] + [L]
+        hs = []
+        for _, d_host in jobs:
+            hs.append([0] + [max(s - self._lead(d_host, 0, s), 0) for s, _ in self.bounds[1:]] + [self.L])
+        nb = len(self.bounds)
 
         def d2h(j):
             """Copy chunk j's outputs back once its kernel is done and, with
             lag, once the input of chunk j + lag has arrived."""
-            s, e = self.bounds[j]
+            jb, s, e = seq[j]
+            ci = j - jb * nb  # chunk index within its job
             ys = max(s - LEAD, 0)
             yb = self.ybuf[j % self.nbuf]
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(comp_ev[j])
                 if j + self.lag < nch:
                     self.s_out.wait_event(in_ev[j + self.lag])
-                self._d2h(d_host, yb, hs[j], hs[j + 1], ys)
+                self._d2h(jobs[jb][1], yb, hs[jb][ci], hs[jb][ci + 1], ys)
                 out_ev[j].record(self.s_out)
 
         launches = 0
-        for idx, (s, e) in enumerate(self.bounds):
+        for idx, (jb, s, e) in enumerate(seq):
+            c_host = jobs[jb][0]
             k = idx % self.nbuf
             xb, yb = self.xbuf[k], self.ybuf[k]
             ys = max(s - LEAD, 0)  # this chunk's outputs [ys, e)
@@ -193,10 +211,13 @@ class ChunkedEntangledConv:
         for st in (self.s_in, self.s_comp, self.s_out):
             st.synchronize()
 
-    def capture(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None):
+    def capture(self, c_host: torch.Tensor, d_host: torch.Tensor, failed: int | None = None,
+                jobs: int = 1):
         """Record the whole job (every copy, kernel and cross-stream event) as
         one CUDA graph on these host buffers; ``replay()`` then costs a single
-        launch instead of ~8 host calls per chunk."""
+        launch instead of ~8 host calls per chunk.  ``jobs`` > 1 records that
+        many back-to-back jobs on the same buffers as one continuous pipeline
+        (``run_many``): a stream of batches, filled and drained once."""
         self.run(c_host, d_host, failed)  # warm: allocator, kernel attributes, tables
         self.synchronize()
         self.graph = torch.cuda.CUDAGraph()
@@ -204,7 +225,7 @@ class ChunkedEntangledConv:
         with torch.cuda.graph(self.graph, stream=cap):
             for st in (self.s_in, self.s_comp, self.s_out):  # fork into the capture
                 st.wait_stream(cap)
-            self.run(c_host, d_host, failed)
+            self.run_many([(c_host, d_host)] * jobs, failed)
             for st in (self.s_in, self.s_comp, self.s_out):  # join back
                 cap.wait_stream(st)
         torch.cuda.synchronize(self.dev)

@@ -491,7 +491,7 @@ def other_configs(D, fused, dev, stream):
         if chain:  # entangle -> scale -> add -> perm as interleave + gather, then conv + extract
             a = torch.from_numpy(wl.add).to(dev)
             add = D.shift_add(a, a, p.l)
-            perm = torch.from_numpy(wl.perm).to(dev)
+            perm = torch.from_numpy(wl.perm).to(dev).to(torch.int32)  # prepared once, like the taps
             xb = xb * abs(wl.scale) + int(add.abs().max())
             ct = torch.empty((n, wl.m), dtype=torch.int32, device=dev)
             xg = torch.empty((wl.m, n), dtype=torch.int32, device=dev)
@@ -507,9 +507,9 @@ def other_configs(D, fused, dev, stream):
 
         def run():
             if chain:
-                from paper_1509_03838_b200._lib import call, ptr, row_ptrs, bits
-                call("nent_interleave", row_ptrs(c), 32, wl.m, n, ptr(ct), D._sh())
-                D.gather_chain(ct, p.l, wl.scale, add, perm, out=xg)
+                # chain words in the coalesced interleave pass, then one record gather
+                D.interleave_chain(c, p.l, wl.scale, add, out=ct)
+                D.gather_records(ct, perm, out=xg)
                 if split:
                     D.conv(xg, gd, K, fl, period=L, n_out=L, out=delta)
                     D.extract_verify(delta, wl.m, p.l, 0, p.w > 32, mm, out=out)

@@ -171,6 +171,17 @@ int nent_chain_conv(const void *a, const void *b, int in_bits, int64_t n_in, int
  *   x[s][p] = scale * ((ct[q][s-1 mod m] << l) + ct[q][s]) + add[q],  q = perm ? perm[p] : p
  * (add may be NULL).  Feed x to nent_fused_conv with pre_entangled = 1. */
 int nent_interleave(const void *const *x, int x_bits, int m, int64_t n, void *out, void *stream);
+/* The same chain with the arithmetic moved into the (coalesced) interleave
+ * pass: nent_interleave_chain writes records of the chain words before the
+ * permutation, out[p*m + s] = scale * ((x[s-1 mod m][p] << l) + x[s][p]) + add[p]
+ * (out_bits == x_bits; the caller's bound must fit), and nent_gather_records
+ * permutes them, x[s][p] = rec[perm[p]][s] (perm int32 or int64), so each
+ * permuted position costs one random record read.  Reference: ops.py:193-204,
+ * 219-220, 250-262. */
+int nent_interleave_chain(const void *const *x, int x_bits, int m, int64_t n, int l, int64_t scale,
+                          const void *add, int add_bits, void *out, int out_bits, void *stream);
+int nent_gather_records(const void *rec, int rec_bits, int m, int64_t n, const void *perm, int perm_bits,
+                        void *const *x, void *stream);
 int nent_gather_chain(const void *ct, int c_bits, int m, int64_t n, int l, int64_t scale,
                       const void *add, int add_bits, const int64_t *perm, void *const *x, int x_bits,
                       void *stream);

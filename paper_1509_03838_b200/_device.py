@@ -316,6 +316,29 @@ def gather_chain(ct: torch.Tensor, l: int, scale: int = 1, add: torch.Tensor | N
     return out
 
 
+def interleave_chain(x: torch.Tensor, l: int, scale: int = 1, add: torch.Tensor | None = None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """(m, n) rows -> (n, m) records of the chain words before the permutation:
+    rec[p, s] = scale * ((x[s-1, p] << l) + x[s, p]) + add[p] (dtype of x; the
+    caller's bound must fit it)."""
+    m, n = x.shape
+    if out is None:
+        out = torch.empty((n, m), dtype=x.dtype, device=x.device)
+    call("nent_interleave_chain", row_ptrs(x), bits(x), m, n, l, int(scale), ptr(add),
+         bits(add) if add is not None else 64, ptr(out), bits(out), _sh())
+    return out
+
+
+def gather_records(rec: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """x[s, p] = rec[perm[p], s]: the permutation of the chain records
+    (perm int32 or int64)."""
+    n, m = rec.shape
+    if out is None:
+        out = torch.empty((m, n), dtype=rec.dtype, device=rec.device)
+    call("nent_gather_records", ptr(rec), bits(rec), m, n, ptr(perm), bits(perm), row_ptrs(out), _sh())
+    return out
+
+
 def elementwise(x: torch.Tensor, g: torch.Tensor, op: int, check: bool, out_dtype=torch.int64):
     rows, n = x.shape
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)

@@ -70,6 +70,8 @@ SIGNATURES = {
                         _P, _P],
     "nent_interleave": [_PP, _I, _I, _L, _P, _P],
     "nent_gather_chain": [_P, _I, _I, _L, _I, _L, _P, _I, _P, _PP, _I, _P],
+    "nent_interleave_chain": [_PP, _I, _I, _L, _I, _L, _P, _I, _P, _I, _P],
+    "nent_gather_records": [_P, _I, _I, _L, _P, _I, _PP, _P],
     "nent_elementwise": [_PP, _I, _I, _L, _P, _I, _L, _I, _PP, _I, _I, _P, _P],
     "nent_scale": [_PP, _I, _I, _L, _L, _PP, _I, _I, _P, _P],
     "nent_permute": [_PP, _I, _I, _L, _P, _PP, _I, _P],

@@ -18,11 +18,26 @@ namespace nent {
 // through shared memory; every thread issues all its row loads (16-byte
 // vectors for int32 rows) before the first store, so ~32 KB per SM are in
 // flight, and writes 16-byte vectors of the position-major output.
-template <typename T>
-__global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m, int64_t n, T* __restrict__ out) {
+//
+// CHAIN: the records hold the chain's words before the permutation instead
+// of the raw samples, out[p*m + s] = scale * ((x[s-1][p] << l) + x[s][p]) +
+// add[p] (int32 when the host's bound says they fit), so the gather after it
+// moves one record per position and nothing else (add no longer a second
+// random read).
+struct ChainArgs {
+  int l;
+  int64_t scale;
+  const void* add;
+  int add_bits;
+};
+
+template <typename T, bool CHAIN = false>
+__global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m, int64_t n, T* __restrict__ out,
+                                                         const ChainArgs ch = ChainArgs{}) {
   constexpr int P = 4096 / sizeof(T);        // positions per tile (1024 int32, 512 int64)
   constexpr int V = 16 / sizeof(T);          // elements per 16-byte vector
   __shared__ T tile[8][P + 16 / sizeof(T)];  // padded rows
+  __shared__ int64_t addt[CHAIN ? P : 1];
   const int tid = threadIdx.x;
   for (int64_t p0 = (int64_t)blockIdx.x * P; p0 < n; p0 += (int64_t)gridDim.x * P) {
     const bool full = p0 + P <= n;
@@ -46,7 +61,18 @@ __global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m, in
         tile[s][j] = p < n ? reinterpret_cast<const T*>(x.p[s])[p] : (T)0;
       }
     }
+    if (CHAIN) {
+      for (int j = tid; j < P; j += blockDim.x)
+        addt[j] = (ch.add && p0 + j < n) ? ld_bits(ch.add, ch.add_bits, p0 + j) : 0;
+    }
     __syncthreads();
+    // record element (position j, stream s) of the tile
+    auto elem = [&](int s, int j) -> T {
+      if (!CHAIN) return tile[s][j];
+      int64_t e = wadd(wshl((int64_t)tile[s == 0 ? m - 1 : s - 1][j], ch.l), (int64_t)tile[s][j]);
+      if (ch.scale != 1) e = wmul(e, ch.scale);
+      return (T)(uint64_t)wadd(e, addt[CHAIN ? j : 0]);
+    };
     // position-major stores: element e = j*m + s of the tile's output span
     const int64_t base = p0 * m;
     const int64_t total = (full ? P : n - p0) * m;
@@ -54,11 +80,11 @@ __global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m, in
       for (int e = V * tid; e < total; e += V * blockDim.x) {
         T v[V];
 #pragma unroll
-        for (int k = 0; k < V; ++k) v[k] = tile[(e + k) % m][(e + k) / m];
+        for (int k = 0; k < V; ++k) v[k] = elem((e + k) % m, (e + k) / m);
         *reinterpret_cast<int4*>(out + base + e) = *reinterpret_cast<const int4*>(v);
       }
     } else {
-      for (int e = tid; e < total; e += blockDim.x) out[base + e] = tile[e % m][e / m];
+      for (int e = tid; e < total; e += blockDim.x) out[base + e] = elem(e % m, e / m);
     }
     __syncthreads();
   }
@@ -113,6 +139,40 @@ gather_chain_kernel(const T* __restrict__ ct, int64_t n, int l, int64_t scale, c
   }
 }
 
+// x_s[p] = rec[q][s], q = perm[p]: the chain words were computed by the
+// CHAIN interleave, so each position is one random record read (one 32-byte
+// sector for 8 int32 streams) and m coalesced stores.  perm int32 or int64.
+template <typename T, int MT, typename TP>
+__global__ void __launch_bounds__(256)
+gather_records_kernel(const T* __restrict__ rec, int64_t n, const TP* __restrict__ perm, MutRows x) {
+  constexpr int GU = 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto one = [&](int64_t pp, int64_t q) {
+    T v[MT];
+    if (sizeof(T) == 4 && MT == 8) {
+      const int4 lo = __ldg(reinterpret_cast<const int4*>(rec + q * MT));
+      const int4 hi = __ldg(reinterpret_cast<const int4*>(rec + q * MT) + 1);
+      const T w[8] = {(T)lo.x, (T)lo.y, (T)lo.z, (T)lo.w, (T)hi.x, (T)hi.y, (T)hi.z, (T)hi.w};
+#pragma unroll
+      for (int s = 0; s < MT; ++s) v[s] = w[s % 8];
+    } else {
+#pragma unroll
+      for (int s = 0; s < MT; ++s) v[s] = __ldg(rec + q * MT + s);
+    }
+#pragma unroll
+    for (int s = 0; s < MT; ++s) reinterpret_cast<T*>(x.p[s])[pp] = v[s];
+  };
+  for (; p + (GU - 1) * stride < n; p += GU * stride) {
+    int64_t q[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) q[u] = (int64_t)__ldg(perm + p + u * stride);
+#pragma unroll
+    for (int u = 0; u < GU; ++u) one(p + u * stride, q[u]);
+  }
+  for (; p < n; p += stride) one(p, (int64_t)__ldg(perm + p));
+}
+
 }  // namespace nent
 
 using namespace nent;
@@ -129,6 +189,56 @@ int nent_interleave(const void* const* x, int x_bits, int m, int64_t n, void* ou
   if (x_bits == 32) interleave_kernel<int32_t><<<grid, 256, 0, s>>>(R, m, n, (int32_t*)out);
   else interleave_kernel<int64_t><<<grid, 256, 0, s>>>(R, m, n, (int64_t*)out);
   return check_launch("interleave");
+}
+
+int nent_interleave_chain(const void* const* x, int x_bits, int m, int64_t n, int l, int64_t scale,
+                          const void* add, int add_bits, void* out, int out_bits, void* stream) {
+  NENT_CHECK_BITS(x_bits);
+  NENT_CHECK_BITS(out_bits);
+  if (add) NENT_CHECK_BITS(add_bits);
+  if (m < 3 || m > 8 || l < 0 || l > 63) { set_error("interleave_chain: bad m=%d l=%d", m, l); return NENT_ERR_PARAM; }
+  if (x_bits != out_bits) { set_error("interleave_chain: x_bits %d != out_bits %d", x_bits, out_bits); return NENT_ERR_PARAM; }
+  if (n == 0) return NENT_OK;
+  Rows R = to_rows(x, m);
+  const ChainArgs ch{l, scale, add, add_bits};
+  const int grid = grid_for(n, x_bits == 32 ? 1024 : 512, 1, 148 * 8);
+  cudaStream_t s = as_stream(stream);
+  if (x_bits == 32) interleave_kernel<int32_t, true><<<grid, 256, 0, s>>>(R, m, n, (int32_t*)out, ch);
+  else interleave_kernel<int64_t, true><<<grid, 256, 0, s>>>(R, m, n, (int64_t*)out, ch);
+  return check_launch("interleave_chain");
+}
+
+int nent_gather_records(const void* rec, int rec_bits, int m, int64_t n, const void* perm, int perm_bits,
+                        void* const* x, void* stream) {
+  NENT_CHECK_BITS(rec_bits);
+  if (m < 3 || m > 8 || !perm || (perm_bits != 32 && perm_bits != 64)) {
+    set_error("gather_records: bad m=%d or perm", m);
+    return NENT_ERR_PARAM;
+  }
+  if (n <= 0) return NENT_OK;
+  MutRows X = to_mrows(x, m);
+  const int grid = grid_for(n, 256, 8);
+  cudaStream_t s = as_stream(stream);
+#define GR(T, MTV)                                                                                     \
+  (perm_bits == 32 ? (gather_records_kernel<T, MTV, int32_t><<<grid, 256, 0, s>>>((const T*)rec, n, (const int32_t*)perm, X), 0) \
+                   : (gather_records_kernel<T, MTV, int64_t><<<grid, 256, 0, s>>>((const T*)rec, n, (const int64_t*)perm, X), 0))
+#define GRM(T)                            \
+  switch (m) {                            \
+    case 3: GR(T, 3); break;              \
+    case 4: GR(T, 4); break;              \
+    case 5: GR(T, 5); break;              \
+    case 6: GR(T, 6); break;              \
+    case 7: GR(T, 7); break;              \
+    default: GR(T, 8); break;             \
+  }
+  if (rec_bits == 32) {
+    GRM(int32_t)
+  } else {
+    GRM(int64_t)
+  }
+#undef GRM
+#undef GR
+  return check_launch("gather_records");
 }
 
 int nent_gather_chain(const void* ct, int c_bits, int m, int64_t n, int l, int64_t scale,

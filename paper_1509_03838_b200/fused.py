@@ -149,7 +149,10 @@ def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: i
     g_dev = D.taps_tensor(g, flavor)
     L = n + K - 1
     if two_pass:
-        x = D.gather_chain(D.interleave(c), p.l, scale, add_ent, perm_dev, out_dtype=torch.int32)
+        # chain words computed in the coalesced interleave pass, then one random
+        # record read per permuted position (int32 indices when they fit)
+        perm_idx = perm_dev.to(torch.int32) if n < (1 << 31) else perm_dev
+        x = D.gather_records(D.interleave_chain(c.to(torch.int32), p.l, scale, add_ent), perm_idx)
         if (is_imma(flavor) and D.imma_kernel(flavor, K, m, True) != "tcgen05"
                 and D.imma_kernel(flavor, K, m, False) == "tcgen05"):
             # m > 3: the fused tensor-core kernel would be the mma.sync one; the

@@ -18,6 +18,7 @@ L = n + K - 1
 a = torch.from_numpy(wl.add).to(dev)
 add = D.shift_add(a, a, p.l)
 perm = torch.from_numpy(wl.perm).to(dev)
+perm32 = perm.to(torch.int32)
 xb = int(np.abs(wl.c).max()) * ((1 << p.l) + 1) * abs(wl.scale) + int(add.abs().max())
 ct = torch.empty((n, m), dtype=torch.int32, device=dev)
 xg = torch.empty((m, n), dtype=torch.int32, device=dev)
@@ -29,6 +30,8 @@ print("params", p, "flavor", MAC_NAMES[fl], "kernel", D.imma_kernel(fl, K, m, Tr
 steps = {
     "interleave": lambda: call("nent_interleave", row_ptrs(c), 32, m, n, ptr(ct), D._sh()),
     "gather_chain": lambda: D.gather_chain(ct, p.l, wl.scale, add, perm, out=xg),
+    "interleave_chain": lambda: D.interleave_chain(c, p.l, wl.scale, add, out=ct),
+    "gather_records32": lambda: D.gather_records(ct, perm32, out=xg),
     "fused_conv": lambda: D.fused_conv(xg, gd, K, p.l, fl, None, True, L, n_in=n, out=out, pre_entangled=True,
                                        imma_table=tab),
 }

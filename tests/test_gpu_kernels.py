@@ -406,3 +406,27 @@ def test_interleave_gather_chain(oracle, m):
         d = D.fused_conv(x.to(torch.int32), D.taps_tensor(g, fl), 40, p.l, fl, 1, False, n + 39,
                          n_in=n, pre_entangled=True)
         assert np.array_equal(d.cpu().numpy(), want), fl
+
+
+@pytest.mark.parametrize("m,n,dt", [(3, 5000, torch.int32), (8, 4099, torch.int32), (8, 1025, torch.int64),
+                                    (5, 333, torch.int32)])
+def test_interleave_chain_gather_records(oracle, m, n, dt):
+    """The chain with its arithmetic in the interleave pass: records of the
+    pre-permutation chain words, then a pure record gather (int32 and int64
+    permutation indices), equal to the oracle's entangle -> scale -> add -> perm."""
+    p = nent.derive_params(m, 32)
+    c = rand(m + 7, (m, n), -100, 100)
+    add = rand(m + 8, (n,), -100, 100)
+    perm = np.random.default_rng(m + n).permutation(n).astype(np.int64)
+    scale = 5
+    eps = oracle.entangle(c, p.l)
+    ent_add = oracle.self_entangle("add", add, p.l)
+    rec_ref = (eps * scale + ent_add).T
+    ref = (eps * scale + ent_add)[:, perm]
+    cd = torch.from_numpy(c).cuda().to(dt)
+    a = torch.from_numpy(add).cuda()
+    rec = D.interleave_chain(cd, p.l, scale, D.shift_add(a, a, p.l))
+    assert rec.dtype == dt and np.array_equal(rec.cpu().numpy(), rec_ref)
+    for pdt in (torch.int32, torch.int64):
+        x = D.gather_records(rec, torch.from_numpy(perm).cuda().to(pdt))
+        assert np.array_equal(x.cpu().numpy(), ref), pdt

@@ -108,9 +108,9 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
     cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     fprintf(stderr, "tc05 timers (kcycles/CTA): mma wait_full %.0f wait_accempty %.0f total %.0f | prod wait_empty %.0f "
-            "wait_cpasync %.0f total %.0f | epi wait_accfull %.0f - total %.0f | setup %.0f max_cta %.0f\n", h[0] / 1e3 / grid,
+            "wait_cpasync %.0f total %.0f | epi wait_accfull %.0f tmem_ld %.0f total %.0f | setup %.0f max_cta %.0f\n", h[0] / 1e3 / grid,
             h[1] / 1e3 / grid, h[2] / 1e3 / grid, h[3] / 1e3 / grid, h[4] / 1e3 / grid, h[5] / 1e3 / grid,
-            h[6] / 1e3 / grid, h[8] / 1e3 / grid, h[9] / 1e3 / grid, h[10] / 1e3);
+            h[6] / 1e3 / grid, h[7] / 1e3 / grid, h[8] / 1e3 / grid, h[9] / 1e3 / grid, h[10] / 1e3);
   }
   return check_launch("tc05 conv");
 }

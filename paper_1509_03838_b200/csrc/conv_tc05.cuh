@@ -24,11 +24,12 @@
 // the A operand from there (kind::i8 with A in TMEM), which leaves shared
 // memory to the digit planes and the raw-input staging.
 //
-// Persistent, warp-specialised CTA (one per SM, 12 warps = 3 per sub-partition):
-//   warp 0      TMEM allocation; one lane issues every tcgen05.mma
-//   warps 1-3   producers: cp.async global -> smem staging (one half-stream
-//               ahead), entangle, digit split -> planes (2 stream slots)
+// Persistent, warp-specialised CTA (one per SM, 16 warps = 4 warpgroups):
+//   warps 0-3, 12-14  producers: TMA bulk copies global -> smem staging (one
+//               half-stream ahead), entangle, digit split -> planes (2 stream slots)
 //   warps 4-11  epilogue: TMEM -> int64 classes -> recovery -> coalesced stores
+//               (NENT_TC05_NEPI=16: warps 4-19, 16 columns each)
+//   warp 15     TMEM allocation; one lane issues every tcgen05.mma
 // TMEM (512 columns): [0,192) taps, [192,512) a ring of 5 accumulator slots
 // of U=64 columns.  Shared memory: two plane slots, the cp.async staging, and
 // the stash of the first stream's int64 result until the second arrives (and
@@ -47,15 +48,29 @@ namespace tcc {
 
 constexpr int U = 64;            // 128-position blocks per tile = MMA N
 constexpr int TILE = 128 * U;    // outputs per tile and stream
-constexpr int NPROD = 7;         // producer warps: 1-3 and 12-15 (16 warps = 4 warpgroups)
-constexpr int NEPI = 8;          // epilogue warps (two per TMEM lane quadrant)
+#ifndef NENT_TC05_NEPI
+#define NENT_TC05_NEPI 8
+#endif
+constexpr int NPROD = 7;         // producer warps: 1-3 and the last warpgroup
+constexpr int NEPI = NENT_TC05_NEPI;  // epilogue warps (NEPI / 4 per TMEM lane quadrant)
+constexpr int EQ = NEPI / 4;     // epilogue warps per lane quadrant
+#ifndef NENT_TC05_MMA_LAST
+#define NENT_TC05_MMA_LAST 1
+#endif
+// The MMA issuer is the CTA's last warp: the warp schedulers favour higher
+// warp ids, so the single thread that feeds the tensor core is not held back
+// by the producer / epilogue warps sharing its sub-partition.
+constexpr int MMA_WARP = NENT_TC05_MMA_LAST ? 4 + NENT_TC05_NEPI + 3 : 0;
 constexpr int NT = 32 * (1 + NPROD + NEPI);
-static_assert(NT == 512, "four warpgroups");
+static_assert(NEPI == 8 || NEPI == 16, "two or four epilogue warpgroups");
 // registers per thread after setmaxnreg: 4 warps x PROD_REGS (issuer + producers,
-// warpgroup 0), 8 x EPI_REGS (epilogue), 4 x PROD_REGS (producers, warpgroup 3)
-// = the 64K register file
-constexpr int PROD_REGS = 88, EPI_REGS = 168;
-static_assert(8 * PROD_REGS + 8 * EPI_REGS <= 2048, "register file");
+// warpgroup 0), NEPI x EPI_REGS (epilogue), 4 x PROD_REGS (producers, last
+// warpgroup).  setmaxnreg.inc draws from the CTA's launch allocation (NT x
+// LAUNCH_REGS), so the split must fit it.  More epilogue warps with fewer
+// outputs each hide the TMEM-load / shared-memory latency of the drain.
+constexpr int LAUNCH_REGS = NEPI == 16 ? 80 : 128;  // 65536 / NT rounded down to 8
+constexpr int PROD_REGS = NEPI == 16 ? 64 : 88, EPI_REGS = NEPI == 16 ? 88 : 168;
+static_assert(8 * PROD_REGS + NEPI * EPI_REGS <= (NT / 32) * LAUNCH_REGS, "launch register pool");
 constexpr int TAPCOLS = 192;     // TMEM columns for the tap table (8 per digit and K step)
 constexpr int RING0 = TAPCOLS;
 constexpr int SLOTS = (512 - RING0) / U;  // accumulator ring: 5 slots of U columns (the
@@ -64,7 +79,8 @@ constexpr int HALFW = 5;         // staged words per producer thread and half-st
 constexpr int PLANE = 9216;      // bytes per digit plane: 128*U + KT - 128 <= 9216, 1024-aligned
 constexpr int NWP = 2 * HALFW * 32 * NPROD;  // plane words every fast tile fills (2240)
 static_assert(4 * NWP <= PLANE, "staging fits one plane");
-constexpr int STASH_BYTES = 32 * NEPI * 32 * 8;  // 32 int64 per epilogue thread
+constexpr int EC = U / EQ;        // accumulator columns (outputs) per epilogue thread and slot
+constexpr int STASH_BYTES = 32 * NEPI * EC * 8;  // EC int64 per epilogue thread
 
 struct Geom {
   int KT;         // GEMM K: K + 127 rounded up to 32
@@ -94,9 +110,19 @@ __device__ __forceinline__ void mb_wait(uint32_t mb, uint32_t parity) {
       "{\n .reg .pred p;\n TC_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra TC_WAIT_%=;\n}" ::"r"(mb), "r"(parity) : "memory");
 }
-// Waits of the producer / epilogue warps: back off between polls so that idle
-// warps do not crowd the MIO queue the MMA issuer also needs.
+// Waits of the producer / epilogue warps.
+#ifndef NENT_TC05_WAIT_HINT
+#define NENT_TC05_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mb_wait_sleep(uint32_t mb, uint32_t parity) {
+#if NENT_TC05_WAIT_HINT
+  // try_wait with a suspend-time hint: the warp is parked in hardware until the
+  // phase completes (or the hint expires) instead of spinning through a
+  // poll / nanosleep loop that costs issue slots on the MMA warp's sub-partition
+  asm volatile(
+      "{\n .reg .pred p;\n TC_WAITH_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra TC_WAITH_%=;\n}" ::"r"(mb), "r"(parity), "r"(0x989680) : "memory");
+#else
   uint32_t done;
   asm volatile(
       "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
@@ -107,6 +133,7 @@ __device__ __forceinline__ void mb_wait_sleep(uint32_t mb, uint32_t parity) {
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done) : "r"(mb), "r"(parity) : "memory");
   }
+#endif
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t e;
@@ -286,6 +313,10 @@ __device__ __forceinline__ void producers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * NPROD) : "memory");
 }
 
+// EC consecutive accumulator columns of this warp's 32 lanes (EC = 16 or 32)
+__device__ __forceinline__ void ld_cols(uint32_t taddr, uint32_t (&r)[32]) { tc05::ld_x32(taddr, r); }
+__device__ __forceinline__ void ld_cols(uint32_t taddr, uint32_t (&r)[16]) { tc05::ld_x16(taddr, r); }
+
 template <bool EXTRACT, int NP, int NG, int NSTEPS>
 __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant__ ConvArgs A,
                                                           const __grid_constant__ Geom G) {
@@ -322,7 +353,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     mb_init(stg_b(1), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) tc05::alloc(&tmem_slot, 512);
+  if (warp == MMA_WARP) tc05::alloc(&tmem_slot, 512);
   tc05::fence_before();
   __syncthreads();
   tc05::fence_after();
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
   else
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PROD_REGS));
 
-  if (warp == 0) {
+  if (warp == MMA_WARP) {
     // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
     {
       const uint32_t idesc = tc05::idesc_i8(128, U, /*b_signed=*/false);
@@ -429,7 +460,9 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     // Work unit: half a stream's words of one tile (HALFW per thread).  The
     // raw words of unit H+1 are in flight (cp.async, thread-private staging)
     // while unit H is entangled and split into digit planes.
-    const int ptid = warp < 4 ? tid - 32 : tid - 32 * (4 + NEPI) + 96;  // 0 .. 32*NPROD-1
+    // 0 .. 32*NPROD-1 over warps 0-3 and the last warpgroup, minus the MMA warp
+    const int ptid = MMA_WARP ? (warp < 4 ? tid : tid - 32 * (4 + NEPI) + 128)
+                              : (warp < 4 ? tid - 32 : tid - 32 * (4 + NEPI) + 96);
     constexpr int PT = 32 * NPROD;
     const uint64_t bias = bias_of(NP);
     const int64_t my_tiles = G.ntiles > blockIdx.x ? (G.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -551,8 +584,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else {
     // ---------------- epilogue ----------------
-    const int ew = warp - 4;  // 0..7
-    const int quad = warp & 3, half = ew >> 2;
+    const int ew = warp - 4;  // 0 .. NEPI-1
+    const int quad = warp & 3, part = ew >> 2;  // lane quadrant, column part of the slot
     const uint32_t lrow = (uint32_t)(32 * quad) << 16;
     const int v = 32 * quad + lane;
     // thread-private stash, [i][epilogue thread] int64: coalesced, conflict-free
@@ -575,9 +608,9 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
       // every output of the tile inside [0, n_out) and int32 rows: unconditional
       // stores at immediate offsets from one per-thread base pointer
       const bool fast = A.y_bits == 32 && A.l < 32 && ybase >= 0 && ybase + TILE <= A.n_out;
-      const int64_t o0 = ybase + 128 * (32 * half) + v;  // this thread's first output
+      const int64_t o0 = ybase + 128 * (EC * part) + v;  // this thread's first output
       for (int q = 0; q < G.nstreams; ++q, cls += NCLS) {
-        uint64_t acc[32];
+        uint64_t acc[EC];
         // classes two at a time (one TMEM round trip per pair).  The loop is
         // unrolled over the compile-time class count, so every class weight
         // 256^c is an immediate: acc += R_c * 256^c is one IMAD.WIDE (c < 4)
@@ -600,10 +633,12 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             TC05_TIMED(0, mb_wait_sleep(accf_b(rs0), (uint32_t)((k0 / SLOTS) & 1)));
             if (two) TC05_TIMED(0, mb_wait_sleep(accf_b(rs1), (uint32_t)(((k0 + 1) / SLOTS) & 1)));
             tc05::fence_after();
-            uint32_t r0[32], r1[32];
-            tc05::ld_x32(tbase + lrow + (uint32_t)(RING0 + rs0 * U + 32 * half), r0);
-            if (two) tc05::ld_x32(tbase + lrow + (uint32_t)(RING0 + rs1 * U + 32 * half), r1);
-            tc05::wait_ld();
+            uint32_t r0[EC], r1[EC];
+            TC05_TIMED(1, {
+              ld_cols(tbase + lrow + (uint32_t)(RING0 + rs0 * U + EC * part), r0);
+              if (two) ld_cols(tbase + lrow + (uint32_t)(RING0 + rs1 * U + EC * part), r1);
+              tc05::wait_ld();
+            });
             tc05::fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -612,12 +647,12 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             }
             if (!two) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) r1[i] = 0;
+              for (int i = 0; i < EC; ++i) r1[i] = 0;
             }
             const int64_t w0 = c < 8 ? (int64_t)((uint64_t)1 << (8 * c)) : 0;
             const int64_t w1 = c + 1 < 8 ? (int64_t)((uint64_t)1 << (8 * (c + 1))) : 0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < EC; ++i) {
               const uint64_t s = (c == 0 ? corr : acc[i]) + (uint64_t)((int64_t)(int32_t)r0[i] * w0);
               acc[i] = s + (uint64_t)((int64_t)(int32_t)r1[i] * w1);
             }
@@ -629,24 +664,24 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           if (fast) {
             int32_t* yo = reinterpret_cast<int32_t*>(yp) + o0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) yo[128 * i] = (int32_t)acc[i];
+            for (int i = 0; i < EC; ++i) yo[128 * i] = (int32_t)acc[i];
           } else {
             const int64_t lim = A.n_out - o0;  // element i is stored iff -o0 <= 128 i < lim
             if (A.y_bits == 32) {
               int32_t* yo = reinterpret_cast<int32_t*>(yp) + o0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
+              for (int i = 0; i < EC; ++i)
                 if (128 * i < lim && 128 * i + o0 >= 0) yo[128 * i] = (int32_t)acc[i];
             } else {
               int64_t* yo = reinterpret_cast<int64_t*>(yp) + o0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
+              for (int i = 0; i < EC; ++i)
                 if (128 * i < lim && 128 * i + o0 >= 0) yo[128 * i] = (int64_t)acc[i];
             }
           }
         } else if (q == 0) {  // delta_{pivot+1}: park it in shared memory
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sts64(stash + SSTEP * i, acc[i]);
+          for (int i = 0; i < EC; ++i) sts64(stash + SSTEP * i, acc[i]);
         } else if (q == 1) {  // delta_{pivot+2}: recover all three, store, park the check word
           void* y0 = A.y.p[pivot];
           void* y1 = A.y.p[pivot + 1 >= 3 ? pivot - 2 : pivot + 1];
@@ -662,7 +697,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             int32_t* z2 = reinterpret_cast<int32_t*>(y2) + o0;
             const int l = A.l;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < EC; ++i) {
               const uint64_t da = lds64(stash + SSTEP * i), db = acc[i];
               const int32_t vv = (int32_t)(((uint32_t)da << l) - (uint32_t)db);
               const int32_t d1 = (int32_t)((int64_t)(db + (uint64_t)(int64_t)vv) >> l);
@@ -675,7 +710,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < EC; ++i) {
               int64_t rot[3], orot[3];
               rot[0] = (int64_t)lds64(stash + SSTEP * i);
               rot[1] = (int64_t)acc[i];
@@ -700,10 +735,10 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
         } else if (A.r < 0) {  // q == 2, verify: the redundant stream against the recovery
           if (fast) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) bad += lds64(stash + SSTEP * i) != acc[i];
+            for (int i = 0; i < EC; ++i) bad += lds64(stash + SSTEP * i) != acc[i];
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < EC; ++i) {
               const int64_t o = o0 + 128 * i;
               if (o >= 0 && o < A.n_out && lds64(stash + SSTEP * i) != acc[i]) ++bad;
             }
@@ -719,8 +754,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
   }
 
 #ifdef NENT_TC05_TIMERS
-  if ((G.debug & 8) && lane == 0 && (warp == 0 || warp == 1 || warp == 4)) {
-    const int role = warp == 0 ? 0 : (warp == 1 ? 1 : 2);
+  if ((G.debug & 8) && lane == 0 && (warp == MMA_WARP || warp == (MMA_WARP ? 0 : 1) || warp == 4)) {
+    const int role = warp == MMA_WARP ? 0 : (warp == 4 ? 2 : 1);
     atomicAdd(G.dbg + 3 * role + 0, (unsigned long long)tw[0]);
     atomicAdd(G.dbg + 3 * role + 1, (unsigned long long)tw[1]);
     atomicAdd(G.dbg + 3 * role + 2, (unsigned long long)(clock64() - tstart));
@@ -732,7 +767,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
 #endif
   tc05::fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == MMA_WARP) {
     tc05::fence_after();
     tc05::dealloc(tbase, 512);
   }

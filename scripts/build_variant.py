@@ -10,7 +10,7 @@ from paper_1509_03838_b200 import _build as B  # noqa: E402
 
 name, defs = sys.argv[1], sys.argv[2:]
 out = Path(__file__).resolve().parent / "_bin"
-obj = out / f"obj_{name}"
+obj = Path("/tmp") / f"nent_variant_obj_{name}"  # objects stay out of the gpurun snapshot
 obj.mkdir(parents=True, exist_ok=True)
 nvcc = B._nvcc()
 

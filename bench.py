@@ -215,8 +215,11 @@ def run_ours(args):
     taps = {f: D.taps_tensor(g, f) for f in {flavor, core_flavor, plain_same, plain_fast, plain_core}}
     # IMMA: digit-split Toeplitz tap tables prepared once (the taps are fixed)
     tables = {f: D.imma_table(taps[f], K, f, y_begin) for f in taps}
-    d_dev = torch.empty((m, n_out), dtype=torch.int32, device=dev)
-    y_plain = torch.empty((m, n_out), dtype=torch.int32, device=dev)
+    # output rows at 128-byte aligned starts (a padded row pitch; the kernels take
+    # one pointer per row), so every warp's 128-byte store is one whole line
+    pitch = (n_out + 31) // 32 * 32
+    d_dev = torch.empty((m, pitch), dtype=torch.int32, device=dev)[:, :n_out]
+    y_plain = torch.empty((m, pitch), dtype=torch.int32, device=dev)[:, :n_out]
     mismatch = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
 

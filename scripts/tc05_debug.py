@@ -19,7 +19,11 @@ g = rng.integers(-2048, 2048, (K,), dtype=np.int64)
 p = nent.derive_params(3, 64)
 fl = imma_flavor(D.signed_digits(2048 * ((1 << p.l) + 1)), D.signed_digits(2048))
 gd = D.taps_tensor(g, fl)
-out = torch.empty((3, n + K - 1), dtype=torch.int32, device="cuda")
+L = n + K - 1
+if os.environ.get("NENT_PAD"):  # 128-byte aligned output rows (padded pitch)
+    out = torch.empty((3, (L + 31) // 32 * 32), dtype=torch.int32, device="cuda")[:, :L]
+else:
+    out = torch.empty((3, L), dtype=torch.int32, device="cuda")
 for dbg in [int(a) for a in sys.argv[1:]] or range(8):
     os.environ["NENT_TC05_DEBUG"] = str(dbg)
     f = lambda: D.fused_conv(x, gd, K, p.l, fl, None, True, n + K - 1, n_in=n, out=out)

@@ -324,47 +324,67 @@ def run_ours(args):
             traffic = None
 
     # ---------------- e2e through the host-buffer path ----------------
+    # Every rank pushes its own host-resident input ([halo | slice] for N > 1)
+    # through the pipeline; the job time is the max over ranks.
     e2e = None
     if world == 1:
-        pipe = ChunkedEntangledConv(params, n, g, flavor)  # 2^20-sample chunks, output lag 1
-        c_host = torch.from_numpy(c_np.astype(np.int32)).pin_memory()
-        d_host = torch.empty((m, n + H), dtype=torch.int32).pin_memory()
-        pipe.capture(c_host, d_host)  # the whole multi-stream job as one CUDA graph
-        d_host.zero_()
+        xin_np = c_np.astype(np.int32)
+    else:
+        xin_np = x_dev.cpu().numpy()  # this rank's staged [halo | slice] words
+    n_e = xin_np.shape[1]
+    pipe = ChunkedEntangledConv(params, n_e, g, flavor)  # 2^20-sample chunks, output lag 1
+    c_host = torch.from_numpy(xin_np).pin_memory()
+    d_host = torch.empty((m, n_e + H), dtype=torch.int32).pin_memory()
+    o0 = 0 if world == 1 else y_begin  # this rank's outputs inside the pipeline's full conv
+
+    def shard_ok() -> bool:
+        return bool(torch.equal(d_host[:, o0:o0 + n_out], d_dev.cpu()))
+
+    pipe.capture(c_host, d_host)  # the whole multi-stream job as one CUDA graph
+    d_host.zero_()
+    pipe.replay()
+    torch.cuda.synchronize(dev)
+    ok = shard_ok()
+    reps = max(3, min(args.steps, 8))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(reps):
         pipe.replay()
         torch.cuda.synchronize(dev)
-        if exact is not None:
-            exact = exact and sha(d_host.to(torch.int64).numpy()) == known
-        reps = max(3, min(args.steps, 8))
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            pipe.replay()
-            torch.cuda.synchronize(dev)
-        single_s = (time.perf_counter() - t0) / reps
-        # streaming: `reps` steps as one continuous pipeline (each step still
-        # copies all its inputs in and all its outputs out; fill/drain once)
-        pipe.capture(c_host, d_host, jobs=reps)
-        d_host.zero_()
-        pipe.replay()
-        torch.cuda.synchronize(dev)
-        if exact is not None:
-            exact = exact and sha(d_host.to(torch.int64).numpy()) == known
-        t0 = time.perf_counter()
-        pipe.replay()
-        torch.cuda.synchronize(dev)
-        e2e_s = (time.perf_counter() - t0) / reps
-        e2e = {"value": m * (n + H) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes(),
-               "d2h_bytes_per_step": pipe.d2h_bytes(), "ms_per_step": e2e_s * 1e3,
-               "steps_streamed": reps, "single_step_ms": single_s * 1e3,
-               "path": "ChunkedEntangledConv: pinned int32 host -> 3-stage pipeline (H2D stream / "
-                       "fused-kernel stream / D2H stream, 2^20-sample chunks each moved as one 2-D DMA "
-                       "per direction, D2H lagging H2D by one chunk, 4-buffer ring, 256-byte-aligned "
-                       "host transfers), "
-                       "the steps captured as one continuous CUDA graph (a stream of batches: the next "
-                       "step's input copies overlap the previous step's last output copies); wall clock "
-                       "over all steps incl. sync; single_step_ms = one step per graph replay + sync",
-               "pcie_floor_ms": "~4.0 (201 MB each way at the ~50 GB/s measured concurrently)",
-               "kernels_per_step": pipe.launches // reps}
+    single_s = (time.perf_counter() - t0) / reps
+    # streaming: `reps` steps as one continuous pipeline (each step still
+    # copies all its inputs in and all its outputs out; fill/drain once)
+    pipe.capture(c_host, d_host, jobs=reps)
+    d_host.zero_()
+    pipe.replay()
+    torch.cuda.synchronize(dev)
+    ok = ok and shard_ok()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    pipe.replay()
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / reps
+    tt = torch.tensor([e2e_s, single_s, 0.0 if ok else 1.0], dtype=torch.float64, device=xdev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s, single_s, bad = (float(v) for v in tt.tolist())
+    if exact is not None:
+        exact = exact and bad == 0.0
+    e2e = {"value": samples_job / e2e_s, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes() * world,
+           "d2h_bytes_per_step": pipe.d2h_bytes() * world, "ms_per_step": e2e_s * 1e3,
+           "steps_streamed": reps, "single_step_ms": single_s * 1e3, "bit_exact_vs_device_output": bad == 0.0,
+           "path": "ChunkedEntangledConv on every rank: pinned int32 host -> 3-stage pipeline (H2D stream / "
+                   "fused-kernel stream / D2H stream, 2^20-sample chunks each moved as one 2-D DMA "
+                   "per direction, D2H lagging H2D by one chunk, 4-buffer ring, 256-byte-aligned "
+                   "host transfers), "
+                   "the steps captured as one continuous CUDA graph (a stream of batches: the next "
+                   "step's input copies overlap the previous step's last output copies); wall clock "
+                   "over all steps incl. sync, max over ranks; single_step_ms = one step per graph "
+                   "replay + sync" + ("; N > 1: each rank's host input is its [halo | slice]" if world > 1 else ""),
+           "pcie_floor_ms": "~4.0 per GPU (201 MB each way at the ~50 GB/s measured concurrently)",
+           "kernels_per_step": pipe.launches // reps}
 
     extras = None
     if rank == 0 and world == 1 and not args.no_extras:
@@ -594,10 +614,19 @@ def host_desc():
     return f"{model} ({os.cpu_count()} logical CPUs, {platform.machine()})"
 
 
+def host_threads() -> int:
+    """Every host thread this process may run on (torchrun exports
+    OMP_NUM_THREADS=1 for N > 1, which would otherwise cap the OpenMP team)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline(c, g, params, target_s: float):
     from oracle import oracle as O
 
-    threads = O.max_threads()
+    threads = host_threads()
     ns = 1 << 16
     t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params, threads)
     ns = int(min(c.shape[1], max(ns, ns * target_s / 2 / max(t, 1e-6))))
@@ -616,7 +645,7 @@ def run_reference(args):
     from oracle import oracle as O
 
     params, c, g = make_inputs(0, 1 << 24, 256)
-    threads = O.max_threads()
+    threads = host_threads()
     ns = 1 << 16  # bounded sample per step, sized so the run stays within a few minutes
     t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params, threads)
     budget = 150.0 / max(args.steps + args.warmup, 1)

@@ -266,6 +266,18 @@ def run_ours(args):
     if world > 1:  # parity of every shard against one single-GPU run over the whole signal
         exact = check_shards(D, d_dev, rank, world, n, K, params, g, flavor, dev, xdev)
 
+    # ---------------- the plain convolutions timed like `value` ----------------
+    # K back-to-back launches each on the same stream, CUDA events around them
+    # (the same protocol as the timed region above)
+    b2b = {"entangled": ms_step}
+    for name, fn in (("plain_same_kernel", lambda: plain(plain_same)),
+                     ("plain_fastest", lambda: plain(plain_fast))):
+        fn()
+        torch.cuda.synchronize(dev)
+        a0, a1 = event_time(fn, stream, args.steps)
+        torch.cuda.synchronize(dev)
+        b2b[name] = a0.elapsed_time(a1) / args.steps
+
     # ---------------- interleaved comparisons (per-launch CUDA events) ----------------
     cands = {
         "entangled": lambda: fused_step(flavor),
@@ -405,8 +417,14 @@ def run_ours(args):
                        "parallelism": "halo-split" if world > 1 else "single GPU",
                        "l2": "inputs 201 MB + outputs 201 MB per step > 126 MB L2; no flush needed",
                        "mac_flavor": MAC_NAMES[flavor], "failed": None, "verify_redundant_stream": True},
-            "overhead_pct": ovh("entangled", "plain_same_kernel"),
+            "overhead_pct": (b2b["entangled"] - b2b["plain_same_kernel"]) / b2b["plain_same_kernel"] * 100,
             "overhead": {
+                "headline": "back-to-back: K launches of the fused entangled kernel (ms_per_step) vs K "
+                            "launches of the same kernel and digit geometry on the plain streams",
+                "back_to_back_ms": b2b,
+                "back_to_back_vs_plain_fastest_pct": (b2b["entangled"] - b2b["plain_fastest"])
+                                                     / b2b["plain_fastest"] * 100,
+                "interleaved_vs_plain_same_kernel_pct": ovh("entangled", "plain_same_kernel"),
                 "vs_plain_same_kernel_pct": ovh("entangled", "plain_same_kernel"),
                 "vs_plain_fastest_pct": ovh("entangled", "plain_fastest"),
                 "cuda_core_entangled_vs_plain_same_width_pct": ovh("entangled_cuda_core",

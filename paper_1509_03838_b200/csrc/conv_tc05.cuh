@@ -61,6 +61,9 @@ constexpr int EQ = NEPI / 4;     // epilogue warps per lane quadrant
 // warp ids, so the single thread that feeds the tensor core is not held back
 // by the producer / epilogue warps sharing its sub-partition.
 constexpr int MMA_WARP = NENT_TC05_MMA_LAST ? 4 + NENT_TC05_NEPI + 3 : 0;
+#ifndef NENT_TC05_ONE_ELECT
+#define NENT_TC05_ONE_ELECT 1
+#endif
 constexpr int NT = 32 * (1 + NPROD + NEPI);
 static_assert(NEPI == 8 || NEPI == 16, "two or four epilogue warpgroups");
 // registers per thread after setmaxnreg: 4 warps x PROD_REGS (issuer + producers,
@@ -419,6 +422,44 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           const int slot = seq & 1;
           if (!(G.debug & 1024)) TC05_TIMED(0, mb_wait(full_b(slot), (uint32_t)((seq >> 1) & 1)));
           if (!(G.debug & 2048)) tc05::fence_after();
+#if NENT_TC05_ONE_ELECT
+          // One elected lane issues the whole stream: every chain's MMAs, the
+          // accumulator-slot waits and the commits, with no warp reconvergence
+          // between the (plane, tap-digit) chains.  The ring position advances
+          // incrementally (no per-chain division).
+          if (elect_one()) {
+            const int rs0 = cls % SLOTS, use0 = cls / SLOTS;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+              const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * NP + p) * PLANE));
+#pragma unroll
+              for (int j = 0; j < NG; ++j) {
+                const int c = p + j;
+                int rs = rs0 + c, use = use0;
+                while (rs >= SLOTS) {
+                  rs -= SLOTS;
+                  ++use;
+                }
+                const bool first = p == (c - NG + 1 > 0 ? c - NG + 1 : 0);
+                if (first && use >= 1 && !(G.debug & 64)) {
+                  TC05_TIMED(1, mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1)));
+                  tc05::fence_after();
+                }
+                const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
+                const uint32_t a = tbase + (uint32_t)(8 * j * NSTEPS);
+                if (!skip) {
+#pragma unroll
+                  for (int kc = 0; kc < NSTEPS; ++kc)
+                    tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
+                }
+                if (p == (c < NP - 1 ? c : NP - 1)) tc05::commit(accf_b(rs));
+              }
+            }
+            if (!(G.debug & 4096)) tc05::commit(empty_b(slot));
+          }
+          __syncwarp();
+          continue;
+#endif
           // fully unrolled: every TMEM / descriptor operand of the chain is then an
           // immediate or a hoisted uniform register (a runtime (p, j) loop rebuilds
           // them with R2UR moves between chains and costs ~30% of the MMA rate)

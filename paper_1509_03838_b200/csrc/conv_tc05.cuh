@@ -364,6 +364,13 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
   // Using the constant keeps every MMA operand in uniform registers.
   if (tmem_slot != 0 || (planes_s & 1023u)) __trap();
   constexpr uint32_t tbase = 0;
+  // Programmatic dependent launch (the host sets the stream-serialization
+  // attribute): the next kernel on the stream may be scheduled from here on --
+  // its CTAs take SMs as ours exit -- and nothing of ours touches global memory
+  // before the previous kernel has completed and flushed.  Without the
+  // attribute both are no-ops.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   {
     // digit bytes of the reversed taps, staged once in shared memory (the
     // cp.async area is still free): rev[j][i] = digit_j(g[KT-1-i]), so that

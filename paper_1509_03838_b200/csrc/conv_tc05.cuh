@@ -651,6 +651,26 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
     const uint64_t corr = 0 - 128 * gsum * ones;
     unsigned bad = 0;
     int64_t cls = 0;
+    // TMEM -> registers for classes k0 (into r0, if first) and k0 + 1 (into r1,
+    // if second) of the ring, then the slots are handed back to the MMA warp
+    uint32_t r0[EC], r1[EC];
+    auto drain = [&](int k0, bool first, bool second) {
+      const int rs0 = k0 % SLOTS, rs1 = (k0 + 1) % SLOTS;
+      if (first) TC05_TIMED(0, mb_wait_sleep(accf_b(rs0), (uint32_t)((k0 / SLOTS) & 1)));
+      if (second) TC05_TIMED(0, mb_wait_sleep(accf_b(rs1), (uint32_t)(((k0 + 1) / SLOTS) & 1)));
+      tc05::fence_after();
+      TC05_TIMED(1, {
+        if (first) ld_cols(tbase + lrow + (uint32_t)(RING0 + rs0 * U + EC * part), r0);
+        if (second) ld_cols(tbase + lrow + (uint32_t)(RING0 + rs1 * U + EC * part), r1);
+        tc05::wait_ld();
+      });
+      tc05::fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (first) mb_arrive(acce_b(rs0));
+        if (second) mb_arrive(acce_b(rs1));
+      }
+    };
     for (int64_t tile = (G.debug & 8192) ? G.ntiles : blockIdx.x; tile < G.ntiles; tile += gridDim.x) {
       const int64_t ybase = tile * TILE - G.shift;  // output index of (u=0, v=0)
       // every output of the tile inside [0, n_out) and int32 rows: unconditional
@@ -677,22 +697,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
         for (int c = 0; c < NCLS; c += 2) {
           {
             const bool two = c + 1 < NCLS;
-            const int k0 = (int)(cls + c), rs0 = k0 % SLOTS, rs1 = (k0 + 1) % SLOTS;
-            TC05_TIMED(0, mb_wait_sleep(accf_b(rs0), (uint32_t)((k0 / SLOTS) & 1)));
-            if (two) TC05_TIMED(0, mb_wait_sleep(accf_b(rs1), (uint32_t)(((k0 + 1) / SLOTS) & 1)));
-            tc05::fence_after();
-            uint32_t r0[EC], r1[EC];
-            TC05_TIMED(1, {
-              ld_cols(tbase + lrow + (uint32_t)(RING0 + rs0 * U + EC * part), r0);
-              if (two) ld_cols(tbase + lrow + (uint32_t)(RING0 + rs1 * U + EC * part), r1);
-              tc05::wait_ld();
-            });
-            tc05::fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              mb_arrive(acce_b(rs0));
-              if (two) mb_arrive(acce_b(rs1));
-            }
+            drain((int)(cls + c), true, two);
             if (!two) {
 #pragma unroll
               for (int i = 0; i < EC; ++i) r1[i] = 0;

@@ -117,6 +117,9 @@ __device__ __forceinline__ void mb_wait(uint32_t mb, uint32_t parity) {
 #ifndef NENT_TC05_WAIT_HINT
 #define NENT_TC05_WAIT_HINT 0
 #endif
+#ifndef NENT_TC05_SLEEP_NS
+#define NENT_TC05_SLEEP_NS 64  // back-off between polls of a not-yet-completed phase
+#endif
 __device__ __forceinline__ void mb_wait_sleep(uint32_t mb, uint32_t parity) {
 #if NENT_TC05_WAIT_HINT
   // try_wait with a suspend-time hint: the warp is parked in hardware until the
@@ -131,7 +134,7 @@ __device__ __forceinline__ void mb_wait_sleep(uint32_t mb, uint32_t parity) {
       "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
       : "=r"(done) : "r"(mb), "r"(parity) : "memory");
   while (!done) {
-    __nanosleep(64);
+    if (NENT_TC05_SLEEP_NS > 0) __nanosleep(NENT_TC05_SLEEP_NS);
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done) : "r"(mb), "r"(parity) : "memory");

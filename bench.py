@@ -461,7 +461,18 @@ def run_ours(args):
                          "cuda_core_path": {"flavor": MAC_NAMES[core_flavor],
                                             "achieved_tflops": 2 * macs_alg / (med["entangled_cuda_core"] / 1e3) / 1e12,
                                             "peak_tflops": 2 * peaks[MAC_NAMES[core_flavor]] / 1e12},
-                         "peaks_measured_gmac_s": {k: v / 1e9 for k, v in peaks.items()}},
+                         "peaks_measured_gmac_s": {k: v / 1e9 for k, v in peaks.items()},
+                         # BASELINE.json north_star's roofline: the 64-bit integer multiply rate
+                         # of the CUDA cores (measured here: IMAD.WIDE and generic 64-bit MAC
+                         # chains); the fused kernel's exact int64 conv MACs (M*N*K) per second
+                         # against it
+                         "int64_cuda_core_roofline": {
+                             "conv_macs_per_s": macs_alg / (kern_ms / 1e3),
+                             "peak_w64_macs_per_s": peaks["w64"], "peak_g64_macs_per_s": peaks["g64"],
+                             "frac_vs_w64": macs_alg / (kern_ms / 1e3) / peaks["w64"],
+                             "frac_vs_g64": macs_alg / (kern_ms / 1e3) / peaks["g64"],
+                             "note": "the tensor-core digit slicing delivers exact 64-bit convolution "
+                                     "MACs faster than the CUDA cores can issue 64-bit multiplies"}},
             "e2e": e2e,
             "gpu_launches": args.steps,  # one fused kernel per step (tap table prepared before)
             "exact": exact,

@@ -61,6 +61,9 @@ constexpr int EQ = NEPI / 4;     // epilogue warps per lane quadrant
 // warp ids, so the single thread that feeds the tensor core is not held back
 // by the producer / epilogue warps sharing its sub-partition.
 constexpr int MMA_WARP = NENT_TC05_MMA_LAST ? 4 + NENT_TC05_NEPI + 3 : 0;
+#ifndef NENT_TC05_SPLIT_STORE
+#define NENT_TC05_SPLIT_STORE 0  // fused m = 3 with the redundant-stream check: d_P stored with the check
+#endif
 #ifndef NENT_TC05_ONE_ELECT
 #define NENT_TC05_ONE_ELECT 1
 #endif
@@ -752,17 +755,34 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             int32_t* z1 = reinterpret_cast<int32_t*>(y1) + o0;
             int32_t* z2 = reinterpret_cast<int32_t*>(y2) + o0;
             const int l = A.l;
+            if (NENT_TC05_SPLIT_STORE && A.r < 0) {
+              // the redundant stream still follows: d_P's store moves to it, so
+              // the stores of one tile are spread 2 + 1 over the last two streams
+              // instead of 3 + 0 (a shorter epilogue burst at this stream, which
+              // the accumulator ring has to absorb).  The stash keeps {d_P, v}.
 #pragma unroll
-            for (int i = 0; i < EC; ++i) {
-              const uint64_t da = lds64(stash + SSTEP * i), db = acc[i];
-              const int32_t vv = (int32_t)(((uint32_t)da << l) - (uint32_t)db);
-              const int32_t d1 = (int32_t)((int64_t)(db + (uint64_t)(int64_t)vv) >> l);
-              const int32_t d0 = (int32_t)((int64_t)(da - (uint64_t)(int64_t)d1) >> l);
-              z0[128 * i] = d0;
-              z1[128 * i] = d1;
-              z2[128 * i] = (int32_t)(0u - (uint32_t)vv);
-              // the pivot stream's word must equal (d_{P+2} << l) + d_P
-              if (A.r < 0) sts64(stash + SSTEP * i, (uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << l));
+              for (int i = 0; i < EC; ++i) {
+                const uint64_t da = lds64(stash + SSTEP * i), db = acc[i];
+                const int32_t vv = (int32_t)(((uint32_t)da << l) - (uint32_t)db);
+                const int32_t d1 = (int32_t)((int64_t)(db + (uint64_t)(int64_t)vv) >> l);
+                const int32_t d0 = (int32_t)((int64_t)(da - (uint64_t)(int64_t)d1) >> l);
+                z1[128 * i] = d1;
+                z2[128 * i] = (int32_t)(0u - (uint32_t)vv);
+                sts64(stash + SSTEP * i, ((uint64_t)(uint32_t)vv << 32) | (uint32_t)d0);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < EC; ++i) {
+                const uint64_t da = lds64(stash + SSTEP * i), db = acc[i];
+                const int32_t vv = (int32_t)(((uint32_t)da << l) - (uint32_t)db);
+                const int32_t d1 = (int32_t)((int64_t)(db + (uint64_t)(int64_t)vv) >> l);
+                const int32_t d0 = (int32_t)((int64_t)(da - (uint64_t)(int64_t)d1) >> l);
+                z0[128 * i] = d0;
+                z1[128 * i] = d1;
+                z2[128 * i] = (int32_t)(0u - (uint32_t)vv);
+                // the pivot stream's word must equal (d_{P+2} << l) + d_P
+                if (A.r < 0) sts64(stash + SSTEP * i, (uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << l));
+              }
             }
           } else {
 #pragma unroll
@@ -789,7 +809,18 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
             }
           }
         } else if (A.r < 0) {  // q == 2, verify: the redundant stream against the recovery
-          if (fast) {
+          if (fast && NENT_TC05_SPLIT_STORE) {
+            // d_P (deferred from the previous stream) and the check of the
+            // redundant word: delta_P == (d_{P+2} << l) + d_P with d_{P+2} = -v
+            int32_t* z0 = reinterpret_cast<int32_t*>(A.y.p[pivot]) + o0;
+#pragma unroll
+            for (int i = 0; i < EC; ++i) {
+              const uint64_t s = lds64(stash + SSTEP * i);
+              const int32_t d0 = (int32_t)(uint32_t)s, vv = (int32_t)(uint32_t)(s >> 32);
+              z0[128 * i] = d0;
+              bad += ((uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << A.l)) != acc[i];
+            }
+          } else if (fast) {
 #pragma unroll
             for (int i = 0; i < EC; ++i) bad += lds64(stash + SSTEP * i) != acc[i];
           } else {

@@ -67,6 +67,9 @@ constexpr int MMA_WARP = NENT_TC05_MMA_LAST ? 4 + NENT_TC05_NEPI + 3 : 0;
 #ifndef NENT_TC05_ONE_ELECT
 #define NENT_TC05_ONE_ELECT 1
 #endif
+#ifndef NENT_TC05_CLASS_MAJOR
+#define NENT_TC05_CLASS_MAJOR 0  // MMA chains in class order (one open accumulator slot) instead of plane order
+#endif
 constexpr int NT = 32 * (1 + NPROD + NEPI);
 static_assert(NEPI == 8 || NEPI == 16, "two or four epilogue warpgroups");
 // registers per thread after setmaxnreg: 4 warps x PROD_REGS (issuer + producers,
@@ -442,6 +445,38 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           // incrementally (no per-chain division).
           if (elect_one()) {
             const int rs0 = cls % SLOTS, use0 = cls / SLOTS;
+#if NENT_TC05_CLASS_MAJOR
+            // class-major: all chains of class c (p + j = c) back to back, then
+            // its commit, so the MMA holds one accumulator slot at a time and
+            // the epilogue gets the rest of the ring as slack (plane-major
+            // order keeps two classes open at once)
+#pragma unroll
+            for (int c = 0; c < NCLS; ++c) {
+              int rs = rs0 + c, use = use0;
+              while (rs >= SLOTS) {
+                rs -= SLOTS;
+                ++use;
+              }
+              if (use >= 1 && !(G.debug & 64)) {
+                TC05_TIMED(1, mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1)));
+                tc05::fence_after();
+              }
+              const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
+#pragma unroll
+              for (int p = (c - NG + 1 > 0 ? c - NG + 1 : 0); p <= (c < NP - 1 ? c : NP - 1); ++p) {
+                const int j = c - p;
+                const bool first = p == (c - NG + 1 > 0 ? c - NG + 1 : 0);
+                const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * NP + p) * PLANE));
+                const uint32_t a = tbase + (uint32_t)(8 * j * NSTEPS);
+                if (!skip) {
+#pragma unroll
+                  for (int kc = 0; kc < NSTEPS; ++kc)
+                    tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
+                }
+              }
+              tc05::commit(accf_b(rs));
+            }
+#else
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
               const uint32_t blo0 = tc05::desc_sw128_lo(planes_s + (uint32_t)((slot * NP + p) * PLANE));
@@ -468,6 +503,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
                 if (p == (c < NP - 1 ? c : NP - 1)) tc05::commit(accf_b(rs));
               }
             }
+#endif
             if (!(G.debug & 4096)) tc05::commit(empty_b(slot));
           }
           __syncwarp();

@@ -620,6 +620,146 @@ def other_configs(D, fused, dev, stream):
     return res
 
 
+# -------------------------------------------------- stream per GPU (cfg3/cfg5) --
+
+def device_barrier(dev, backend, group=None):
+    """Cross-rank ordering of device work: with NCCL a one-element all-reduce
+    on the current stream (every rank's earlier kernels complete before any
+    rank's later ones run; no host sync); with gloo (ranks sharing one GPU in
+    the CPU-side tests) a device sync plus a host barrier."""
+    import torch
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        dist.all_reduce(torch.zeros(1, device=dev), group=group)
+    else:
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+
+def run_stream_per_gpu(cfg: int, steps: int, warmup: int, dev, backend: str) -> dict | None:
+    """BASELINE cfg3 (M=4) / cfg5 (M=8) with one entangled stream per GPU
+    (reference pipeline.py:90-137): rank i holds c_i; one step
+    = ring shift of c_{i-1} (P2P), the worker's fused entangle [-> scale ->
+    add -> permute] -> conv kernel giving delta_i, the drop of rank
+    r = step mod M (every GPU fails in turn), and the position-sharded K3 on
+    every survivor reading its slice of the other survivors' deltas straight
+    from their HBM (CUDA IPC peer pointers over NVLink).  Reported: recovered
+    output samples/s of the job (max over ranks), the plain per-GPU
+    convolution (no entanglement, no recovery) timed the same way, the
+    recovery alone, and the reference digest of the recovered outputs for
+    every dropped rank (gathered to rank 0)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_03838_b200 import _device as D
+    from paper_1509_03838_b200 import workloads
+    from paper_1509_03838_b200._lib import MAC_NAMES
+    from paper_1509_03838_b200.distributed import PeerRows, StreamPerGPU
+    from paper_1509_03838_b200.fused import chain_operands, conv_flavor
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    wl = workloads.make(cfg)
+    p, m, n, K = wl.params, wl.m, wl.n, wl.K
+    if world != m:
+        return None
+    L = n + K - 1
+    drv = StreamPerGPU(p)
+    c_own = torch.from_numpy(wl.c[rank].copy()).to(dev).to(torch.int32)
+    chain = wl.scale is not None
+    add_ent = perm = None
+    xb = int(np.abs(wl.c).max()) * ((1 << p.l) + 1)
+    if chain:
+        add_dev, perm = chain_operands(wl.add, wl.perm, n)
+        add_ent = D.shift_add(add_dev.to(torch.int32), add_dev.to(torch.int32), p.l, out_dtype=torch.int32)
+        xb = xb * abs(wl.scale) + int(np.abs(wl.add).max()) * ((1 << p.l) + 1)
+    flavor = conv_flavor(xb, wl.g, n_out=L, gather=chain)
+    plain_flavor = conv_flavor(int(np.abs(wl.c).max()) * (abs(wl.scale) if chain else 1)
+                               + (int(np.abs(wl.add).max()) if chain else 0), wl.g, n_out=L, gather=chain)
+    g_dev = D.taps_tensor(wl.g, flavor)
+    gp_dev = D.taps_tensor(wl.g, plain_flavor)
+    tab = D.imma_table(g_dev, K, flavor, 0)
+    ptab = D.imma_table(gp_dev, K, plain_flavor, 0)
+    sum_g = int(np.abs(wl.g).sum())
+    ddt = torch.int32 if xb * sum_g < (1 << 31) else torch.int64
+    delta = torch.empty((L,), dtype=ddt, device=dev)
+    y_plain = torch.empty((1, L), dtype=torch.int32, device=dev)
+    add_plain = torch.from_numpy(wl.add).to(dev).to(torch.int32) if chain else None
+    # the survivors' rows, mapped once (the buffer is persistent across steps)
+    rows = PeerRows(drv, delta)
+    width = -(-L // (m - 1))
+    d_out = torch.empty((m, width), dtype=torch.int32, device=dev)
+
+    def worker():
+        prev = drv.ring_shift(c_own)
+        D.chain_conv(prev, c_own, g_dev, K, p.l, flavor, L, n_in=n, scale=wl.scale or 1, add=add_ent,
+                     perm=perm, out=delta, imma_table=tab)
+
+    def recover(failed):
+        mb, me = rows.bounds(failed)
+        if me > mb:
+            rows.extract(failed, out=d_out[:, : me - mb])
+
+    def step(s):
+        worker()
+        device_barrier(dev, backend)   # every delta complete before any peer read
+        recover(s % m)
+        device_barrier(dev, backend)   # every read done before the next step rewrites delta
+
+    def plain():
+        D.chain_conv(None, c_own, gp_dev, K, p.l, plain_flavor, L, n_in=n, scale=wl.scale or 1,
+                     add=add_plain, perm=perm, out=y_plain[0], imma_table=ptab)
+
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, k):
+        device_barrier(dev, backend)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(k):
+            fn(i)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([a.elapsed_time(b) / k], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(warmup):
+        step(i)
+        plain()
+    ms_ent = timed(step, steps)
+    ms_plain = timed(lambda i: plain(), steps)
+    worker()
+    device_barrier(dev, backend)
+    ms_rec = timed(lambda i: recover(i % m), steps)
+    ms_worker = timed(lambda i: worker(), steps)
+    device_barrier(dev, backend)
+    # parity: the recovered outputs of every dropped rank against the reference digest
+    want = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())[f"cfg{cfg}"]["d"]
+    exact = {}
+    for r in list(range(m)) + [None]:
+        d, mb, me = rows.extract(r)
+        full = drv.gather(d, L, r, dst=0)
+        if rank == 0:
+            exact[str(r)] = sha(full.to(torch.int64).cpu().numpy()) == want
+        del full, d
+    rows.close()
+    samples = m * L
+    return {"workload": f"cfg{cfg}: M={m} streams of N={n}, K={K}, (m,w,l,k)=({p.m},{p.w},{p.l},{p.k})"
+                        + (f", chain scale {wl.scale} -> add -> perm -> conv" if chain else ", full conv"),
+            "parallelism": f"stream-per-GPU ({m} ranks, one entangled stream each)",
+            "ms_per_step": ms_ent, "value": samples / (ms_ent / 1e3), "unit": UNIT,
+            "plain_ms_per_step": ms_plain, "plain_value": samples / (ms_plain / 1e3),
+            "overhead_pct": (ms_ent - ms_plain) / ms_plain * 100,
+            "worker_ms": ms_worker, "recovery_ms": ms_rec,
+            "recovery_note": "K3 on each survivor's 1/(M-1) slice reading the other survivors' deltas in place "
+                             "(CUDA IPC peer pointers), dropped rank = step mod M",
+            "flavor": MAC_NAMES[flavor], "plain_flavor": MAC_NAMES[plain_flavor],
+            "exact_every_dropped_rank": exact if rank == 0 else None,
+            "backend": backend}
+
+
 # ------------------------------------------------------------- CPU baseline --
 
 def cpu_pipeline_time(O, c: np.ndarray, g: np.ndarray, params, threads: int = 0):

@@ -68,6 +68,11 @@ int nent_imma_kernel(int flavor, int K, int rows, int extract);
 
 const char *nent_last_error(void);
 int nent_abi_version(void);
+/* Lets kernels on the current device dereference memory of device `peer`
+ * (NVLink peer access; already-enabled is not an error).  The multi-GPU
+ * recovery passes peer rows (CUDA IPC-mapped deltas of other ranks) to
+ * nent_extract. */
+int nent_enable_peer_access(int peer);
 /* 1 if the library was compiled for and can launch on the current device. */
 int nent_device_ok(void);
 
@@ -182,6 +187,12 @@ int nent_interleave_chain(const void *const *x, int x_bits, int m, int64_t n, in
                           const void *add, int add_bits, void *out, int out_bits, void *stream);
 int nent_gather_records(const void *rec, int rec_bits, int m, int64_t n, const void *perm, int perm_bits,
                         void *const *x, void *stream);
+/* Kernel.of_permutation's bijection check (ops.py:57-62) on the device:
+ * *bad_dev += number of indices outside [0, n) plus repeated indices, so 0
+ * means perm is a bijection of [0, n).  bitmap: caller-zeroed workspace of
+ * ceil(n / 32) uint32 words.  perm int32 or int64. */
+int nent_perm_check(const void *perm, int perm_bits, int64_t n, unsigned *bitmap, unsigned long long *bad_dev,
+                    void *stream);
 int nent_gather_chain(const void *ct, int c_bits, int m, int64_t n, int l, int64_t scale,
                       const void *add, int add_bits, const int64_t *perm, void *const *x, int x_bits,
                       void *stream);

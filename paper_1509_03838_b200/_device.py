@@ -339,6 +339,28 @@ def gather_records(rec: torch.Tensor, perm: torch.Tensor, out: torch.Tensor | No
     return out
 
 
+def enable_peer_access(peer: int) -> None:
+    """Kernels on the current device may then read device ``peer``'s memory."""
+    call("nent_enable_peer_access", int(peer))
+
+
+def perm_check(perm: torch.Tensor) -> None:
+    """Kernel.of_permutation's bijection test (ops.py:57-62) on the device;
+    raises ParameterError unless ``perm`` is a permutation of [0, len)."""
+    if perm.dim() != 1:
+        raise ParameterError("permutation kernel is not a bijection")
+    n = perm.numel()
+    if n == 0:
+        return
+    if perm.dtype not in (torch.int32, torch.int64):
+        perm = perm.to(torch.int64)
+    bitmap = torch.zeros(((n + 31) // 32,), dtype=torch.int32, device=perm.device)
+    bad = _status()
+    call("nent_perm_check", ptr(perm), bits(perm), n, ptr(bitmap), ptr(bad), _sh())
+    if int(bad.item()):
+        raise ParameterError("permutation kernel is not a bijection")
+
+
 def elementwise(x: torch.Tensor, g: torch.Tensor, op: int, check: bool, out_dtype=torch.int64):
     rows, n = x.shape
     out = torch.empty((rows, n), dtype=out_dtype, device=x.device)

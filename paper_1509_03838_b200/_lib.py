@@ -57,6 +57,7 @@ SIGNATURES = {
     "nent_last_error": [],
     "nent_abi_version": [],
     "nent_device_ok": [],
+    "nent_enable_peer_access": [_I],
     "nent_entangle": [_PP, _I, _PP, _I, _I, _L, _I, _L, _P, _P],
     "nent_shift_add": [_P, _P, _I, _P, _I, _L, _I, _P],
     "nent_extract": [_PP, _I, _PP, _I, _I, _L, _I, _I, _I, _P, _P],
@@ -72,6 +73,7 @@ SIGNATURES = {
     "nent_gather_chain": [_P, _I, _I, _L, _I, _L, _P, _I, _P, _PP, _I, _P],
     "nent_interleave_chain": [_PP, _I, _I, _L, _I, _L, _P, _I, _P, _I, _P],
     "nent_gather_records": [_P, _I, _I, _L, _P, _I, _PP, _P],
+    "nent_perm_check": [_P, _I, _L, _P, _P, _P],
     "nent_elementwise": [_PP, _I, _I, _L, _P, _I, _L, _I, _PP, _I, _I, _P, _P],
     "nent_scale": [_PP, _I, _I, _L, _L, _PP, _I, _I, _P, _P],
     "nent_permute": [_PP, _I, _I, _L, _P, _PP, _I, _P],

@@ -60,11 +60,22 @@ def entangle(block: StreamBlock, counters: OpCounters | None = None) -> Entangle
     return _wrap(block, p, eps, host, EntangledBlock)
 
 
+def _store_back(dst: torch.Tensor, src: torch.Tensor, what: str) -> None:
+    """Copy ``src`` (int64) into the block's own device buffer.  An int32
+    buffer cannot hold words that leave int32 (torch's copy_ would silently
+    keep the low 32 bits; the reference's blocks are always int64), so that
+    case raises instead."""
+    if dst.dtype == torch.int32 and src.numel() and D.max_abs(src.reshape(src.shape[0], -1)) > (1 << 31) - 1:
+        raise ParameterError(f"{what} words do not fit the block's int32 buffer; "
+                             "use an int64 device block (or the copying variant)")
+    dst.copy_(src)
+
+
 def entangle_inplace(block: StreamBlock, counters: OpCounters | None = None) -> EntangledBlock:
     """Entangle overwriting ``block``'s buffer; the result shares it (codec.py:75-79)."""
     ent = entangle(block, counters)
     if block.on_device:
-        block.data.copy_(ent.data)
+        _store_back(block.data, ent.data, "entangled")
     else:
         block.data[...] = ent.data
     return EntangledBlock(block.params, block.data)
@@ -95,7 +106,7 @@ def disentangle_inplace(block: EntangledBlock, failed: int | None = None,
                         counters: OpCounters | None = None) -> StreamBlock:
     rec = disentangle(block, failed, counters)
     if block.on_device:
-        block.data.copy_(rec.data)
+        _store_back(block.data, rec.data, "recovered")
     else:
         block.data[...] = rec.data
     return StreamBlock(block.params, block.data)

@@ -173,6 +173,30 @@ gather_records_kernel(const T* __restrict__ rec, int64_t n, const TP* __restrict
   for (; p < n; p += stride) one(p, (int64_t)__ldg(perm + p));
 }
 
+// Kernel.of_permutation's bijection test (ops.py:57-62, sorted(idx) == range(n))
+// on the device: every index must lie in [0, n) and be hit once.  bitmap is a
+// caller-zeroed workspace of ceil(n / 32) words; *bad_dev counts out-of-range
+// indices plus repeats (0 <=> bijection, since n in-range distinct indices
+// cover [0, n)).
+template <typename TP>
+__global__ void __launch_bounds__(256) perm_check_kernel(const TP* __restrict__ perm, int64_t n,
+                                                          unsigned* __restrict__ bitmap,
+                                                          unsigned long long* __restrict__ bad) {
+  unsigned long long nbad = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = (int64_t)perm[j];
+    if (v < 0 || v >= n) {
+      ++nbad;
+      continue;
+    }
+    const unsigned bit = 1u << (v & 31);
+    if (atomicOr(bitmap + (v >> 5), bit) & bit) ++nbad;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nbad += __shfl_xor_sync(0xffffffffu, nbad, o);
+  if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(bad, nbad);
+}
+
 }  // namespace nent
 
 using namespace nent;
@@ -265,6 +289,22 @@ int nent_gather_chain(const void* ct, int c_bits, int m, int64_t n, int l, int64
   }
 #undef GC
   return check_launch("gather_chain");
+}
+
+int nent_perm_check(const void* perm, int perm_bits, int64_t n, unsigned* bitmap, unsigned long long* bad_dev,
+                    void* stream) {
+  if (!perm || !bitmap || !bad_dev || (perm_bits != 32 && perm_bits != 64)) {
+    set_error("perm_check: bad arguments");
+    return NENT_ERR_PARAM;
+  }
+  if (n <= 0) return NENT_OK;
+  const int grid = grid_for(n, 256, 4);
+  cudaStream_t s = as_stream(stream);
+  if (perm_bits == 32)
+    perm_check_kernel<int32_t><<<grid, 256, 0, s>>>((const int32_t*)perm, n, bitmap, bad_dev);
+  else
+    perm_check_kernel<int64_t><<<grid, 256, 0, s>>>((const int64_t*)perm, n, bitmap, bad_dev);
+  return check_launch("perm_check");
 }
 
 }  // extern "C"

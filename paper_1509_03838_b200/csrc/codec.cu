@@ -213,6 +213,22 @@ extern "C" {
 const char* nent_last_error(void) { return g_err; }
 int nent_abi_version(void) { return NENT_ABI_VERSION; }
 
+int nent_enable_peer_access(int peer) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { set_error("no CUDA device"); return NENT_ERR_CUDA; }
+  if (peer == dev) return NENT_OK;
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, dev, peer);
+  if (!can) { set_error("device %d cannot access device %d", dev, peer); return NENT_ERR_CUDA; }
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+    set_error("cudaDeviceEnablePeerAccess(%d): %s", peer, cudaGetErrorString(e));
+    return NENT_ERR_CUDA;
+  }
+  cudaGetLastError();  // clear a sticky "already enabled"
+  return NENT_OK;
+}
+
 int nent_device_ok(void) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) { set_error("no CUDA device"); return 0; }

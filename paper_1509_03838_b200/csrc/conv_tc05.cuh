@@ -288,27 +288,61 @@ __device__ __forceinline__ int tile_mode(const ConvArgs& A, int row, int64_t P0)
 // HALFB bytes), then the a operand's.  Thread ptid reads int4 i*PT + ptid.
 constexpr uint32_t HALFB = HALFW * 32 * NPROD * 16;
 
+// NP <= 4: the 4 digit planes of 4 consecutive 32-bit words u (bytes =
+// unsigned digits), one 32-bit word per plane.
+template <int NP>
+__device__ __forceinline__ void put4_32(uint32_t addr, uint32_t u0, uint32_t u1, uint32_t u2, uint32_t u3) {
+  uint32_t o[4];
+  transpose4(u0, u1, u2, u3, o);
+#pragma unroll
+  for (int p = 0; p < NP; ++p) sts32(addr + (uint32_t)(p * PLANE), o[p]);
+}
+
 template <int NP, bool ENT>
 __device__ __forceinline__ void fill_half(uint32_t st, uint32_t pl, uint32_t w0, uint64_t bias, int l) {
   constexpr int PT = 32 * NPROD;
+  // every staged vector of the unit is loaded before any is used (plain,
+  // non-volatile loads the compiler may batch): one shared-memory latency per
+  // unit instead of one per vector
+  int4 bv[HALFW], av[HALFW];
+  const int4* sb = reinterpret_cast<const int4*>(__cvta_shared_to_generic(st));
 #pragma unroll
   for (int i = 0; i < HALFW; ++i) {
-    const int4 bv = lds128(st + (uint32_t)(i * PT) * 16u);
-    uint64_t u[4] = {(uint64_t)(int64_t)bv.x + bias, (uint64_t)(int64_t)bv.y + bias, (uint64_t)(int64_t)bv.z + bias,
-                     (uint64_t)(int64_t)bv.w + bias};
-    if (ENT) {
-      // + (a << l) as a {lo, hi} pair: the high word is a >> (32 - l) directly
-      // (l in [1, 31], checked on the host), so each position costs one shift
-      // pair and one 64-bit add
-      const int4 av = lds128(st + HALFB + (uint32_t)(i * PT) * 16u);
-      const int av4[4] = {av.x, av.y, av.z, av.w};
+    bv[i] = sb[i * PT];
+    if (ENT) av[i] = sb[HALFB / 16 + i * PT];
+  }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint64_t sh = ((uint64_t)(uint32_t)(av4[e] >> (32 - l)) << 32) | (uint32_t)((uint32_t)av4[e] << l);
-        u[e] += sh;
+  for (int i = 0; i < HALFW; ++i) {
+    const uint32_t dst = pl + tc05::sw128(4u * (w0 + (uint32_t)(PT * i)));
+    if (NP <= 4) {
+      // the words fit 32 bits (NP balanced digits): u = b + (a << l) + bias
+      // modulo 2^32 has the unsigned digits as its bytes
+      const uint32_t b32 = (uint32_t)bias;
+      uint32_t u[4] = {(uint32_t)bv[i].x + b32, (uint32_t)bv[i].y + b32, (uint32_t)bv[i].z + b32,
+                       (uint32_t)bv[i].w + b32};
+      if (ENT) {
+        u[0] += (uint32_t)av[i].x << l;
+        u[1] += (uint32_t)av[i].y << l;
+        u[2] += (uint32_t)av[i].z << l;
+        u[3] += (uint32_t)av[i].w << l;
       }
+      put4_32<NP>(dst, u[0], u[1], u[2], u[3]);
+    } else {
+      uint64_t u[4] = {(uint64_t)(int64_t)bv[i].x + bias, (uint64_t)(int64_t)bv[i].y + bias,
+                       (uint64_t)(int64_t)bv[i].z + bias, (uint64_t)(int64_t)bv[i].w + bias};
+      if (ENT) {
+        // + (a << l) as a {lo, hi} pair: the high word is a >> (32 - l) directly
+        // (l in [1, 31], checked on the host), so each position costs one shift
+        // pair and one 64-bit add
+        const int av4[4] = {av[i].x, av[i].y, av[i].z, av[i].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint64_t sh = ((uint64_t)(uint32_t)(av4[e] >> (32 - l)) << 32) | (uint32_t)((uint32_t)av4[e] << l);
+          u[e] += sh;
+        }
+      }
+      put4<NP>(dst, u);
     }
-    put4<NP>(pl + tc05::sw128(4u * (w0 + (uint32_t)(PT * i))), u);
   }
 }
 

@@ -14,9 +14,13 @@ the plumbing:
        nothing) gives each survivor the surviving deltas of its slice, and K3
        recovers all M outputs there;
     5. optional gather of the recovered slices.
-  ``recover_peer`` is the fused alternative for a single node: every rank
-  exports its delta buffer through CUDA IPC and the extract kernel reads the
-  survivors' slices straight out of peer HBM over NVLink (no staging copy).
+  ``recover_peer`` is the fused alternative for a single node: every
+  surviving rank exports its delta buffer as a CUDA IPC handle (exchanged as
+  a few bytes over the process group), and each survivor's K3 launch takes
+  the other survivors' rows as peer pointers, so the extract kernel reads its
+  1/(M-1) slice of every surviving delta straight out of peer HBM over NVLink
+  (no staging copy, no collective on the data path; the failed rank exports
+  nothing and nothing of it is read).
 
 * ``HaloSplit`` -- a long signal cut into contiguous slices; rank p needs the
   K-1 samples left of its slice from rank p-1 (one P2P exchange), then runs the
@@ -25,7 +29,11 @@ the plumbing:
 
 Compute goes through a ``compute`` object (default ``DeviceCompute``: the
 sm_100a kernels); the CPU tests inject a CPU stand-in to exercise the
-exchange logic under gloo.
+exchange logic under gloo, and the GPU tests run ``DeviceCompute`` with
+several ranks sharing one device (gloo exchanges through host memory).
+
+Peers are given as group-local ranks (``group_peer`` / ``group_dst``), so any
+sub-group of the world works, not only WORLD.
 """
 
 from __future__ import annotations
@@ -51,8 +59,11 @@ class DeviceCompute:
         from . import _device as D
         from .fused import conv_flavor
 
+        from .fused import chain_operands
+
         n = c_own.shape[-1]
         K = len(g)
+        add, perm = chain_operands(add, perm, n)  # LsbOp.validate / Kernel.of_permutation
         flavor = self.flavor
         if flavor is None:
             mc = max(D.max_abs(c_own.reshape(1, -1)), D.max_abs(c_prev.reshape(1, -1)))
@@ -87,6 +98,15 @@ class DeviceCompute:
                             n_in=n_in, y_begin=y_begin, n_out=n_out)
 
 
+def _host_exchange(group) -> bool:
+    """gloo moves CPU tensors only: device data is staged through host memory."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _to_x(t: torch.Tensor, group) -> torch.Tensor:
+    return t.cpu() if (t.is_cuda and _host_exchange(group)) else t
+
+
 def shard_bounds(L: int, parts: int, idx: int) -> tuple[int, int]:
     """[begin, end) of slice ``idx`` when L positions are cut into ``parts``
     near-equal contiguous slices (the first L % parts get one extra)."""
@@ -114,12 +134,13 @@ class StreamPerGPU:
     def ring_shift(self, c_own: torch.Tensor) -> torch.Tensor:
         """Return c_{rank-1} (the stream entangled into this rank's word)."""
         m = self.world
-        prev = torch.empty_like(c_own)
-        ops = [dist.P2POp(dist.isend, c_own.contiguous(), (self.rank + 1) % m, self.group),
-               dist.P2POp(dist.irecv, prev, (self.rank - 1) % m, self.group)]
+        send = _to_x(c_own.contiguous(), self.group)
+        prev = torch.empty_like(send)
+        ops = [dist.P2POp(dist.isend, send, group=self.group, group_peer=(self.rank + 1) % m),
+               dist.P2POp(dist.irecv, prev, group=self.group, group_peer=(self.rank - 1) % m)]
         for w in dist.batch_isend_irecv(ops):
             w.wait()
-        return prev
+        return prev.to(c_own.device)
 
     # -- 2. worker ------------------------------------------------------------
     def work(self, c_own: torch.Tensor, g, scale: int = 1, add=None, perm=None,
@@ -155,9 +176,10 @@ class StreamPerGPU:
                 recv_sizes[src] = me - mb
         else:
             mb = me = 0
-        send = delta_local.contiguous() if me_alive else delta_local.new_empty(0)
-        recv = delta_local.new_empty(sum(recv_sizes))
+        send = _to_x(delta_local.contiguous() if me_alive else delta_local.new_empty(0), self.group)
+        recv = send.new_empty(sum(recv_sizes))
         dist.all_to_all_single(recv, send.reshape(-1), recv_sizes, send_sizes, group=self.group)
+        recv = recv.to(delta_local.device)
         if not me_alive:
             return delta_local.new_empty((m, 0)), 0, 0
         width = me - mb
@@ -183,15 +205,34 @@ class StreamPerGPU:
         buf = d_slice.new_zeros((m, maxw))
         if d_slice.shape[-1]:
             buf[:, : d_slice.shape[-1]] = d_slice
+        buf = _to_x(buf, self.group)
         parts = [torch.empty_like(buf) for _ in range(m)] if self.rank == dst else None
-        dist.gather(buf, parts, dst=dst, group=self.group)
+        dist.gather(buf, parts, group=self.group, group_dst=dst)
         if self.rank != dst:
             return None
         out = d_slice.new_empty((m, L))
         for k, src in enumerate(surv):
             b, e = shard_bounds(L, nsurv, k)
-            out[:, b:e] = parts[src][:, : e - b]
+            out[:, b:e] = parts[src][:, : e - b].to(out.device)
         return out
+
+    # -- 4'. fused peer-read recovery (one node, CUDA IPC over NVLink) ---------
+    def recover_peer(self, delta_local: torch.Tensor, failed: int | None):
+        """Position-sharded recovery reading the survivors' deltas in place.
+
+        Every survivor exports its (L,) delta through CUDA IPC; the handles
+        (a few bytes each) travel over the process group; survivor i opens the
+        others' buffers and runs K3 (``nent_extract``) on positions
+        [b_i, e_i) with row pointers straight into peer HBM -- the rows of
+        ``codec.disentangle`` (codec.py:110-131, _kernels.py:33-67) are
+        separate GPUs' memory here and the kernel never touches row ``failed``
+        (the failed rank does not even export its buffer).  A barrier keeps
+        every exported buffer alive until all reads are done.
+        Returns (d_slice (m, e-b), b, e); the failed rank gets an empty slice."""
+        rows = PeerRows(self, delta_local, exclude=failed)
+        d, mb, me = rows.extract(failed)
+        rows.close()
+        return d, mb, me
 
     def run(self, c_own: torch.Tensor, g, failed: int | None = None, scale: int = 1, add=None,
             perm=None, full: bool = True, dst: int | None = 0):
@@ -202,6 +243,74 @@ class StreamPerGPU:
         if dst is None:
             return d, b, e
         return self.gather(d, int(delta.shape[-1]), failed, dst)
+
+
+class PeerRows:
+    """The M ranks' delta buffers mapped into every rank (CUDA IPC), opened
+    once for a persistent buffer so repeated recoveries cost one K3 launch.
+
+    ``exclude`` (a failed rank) exports nothing.  ``extract(failed)`` runs K3
+    on this rank's 1/(M-1) position slice with the survivors' rows as peer
+    pointers; ``close()`` is collective (the owners may then free or rewrite
+    their buffers).  Callers order the kernels across ranks: every owner's
+    delta must be complete before any rank's extract reads it, and no owner
+    rewrites its buffer before every extract of the step is done (bench.py
+    uses one tiny NCCL all-reduce on each side; ``recover_peer`` host
+    barriers)."""
+
+    def __init__(self, drv: "StreamPerGPU", delta_local: torch.Tensor, exclude: int | None = None):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import _device as D
+
+        if not delta_local.is_cuda:
+            raise ParameterError("peer-read recovery needs device-resident deltas")
+        self.drv, self.local = drv, delta_local.reshape(-1)
+        self.L = int(self.local.numel())
+        torch.cuda.current_stream(delta_local.device).synchronize()  # the exported data is complete
+        mine = reduce_tensor(self.local) if drv.rank != exclude else None
+        shared = [None] * drv.world
+        dist.all_gather_object(shared, mine, group=drv.group)
+        self.rows = [None] * drv.world
+        for j, h in enumerate(shared):
+            if h is None:
+                continue
+            if j == drv.rank:
+                self.rows[j] = self.local
+                continue
+            fn, args = h
+            t = fn(*args)  # rank j's buffer, mapped from its GPU (NVLink) or the same device
+            if t.device != delta_local.device:
+                D.enable_peer_access(t.device.index)
+            self.rows[j] = t.reshape(-1)
+
+    def bounds(self, failed: int | None) -> tuple[int, int]:
+        surv = self.drv.survivors(failed)
+        if self.drv.rank not in surv:
+            return 0, 0
+        return shard_bounds(self.L, len(surv), surv.index(self.drv.rank))
+
+    def extract(self, failed: int | None, out: torch.Tensor | None = None):
+        from . import _device as D
+
+        m = self.drv.world
+        mb, me = self.bounds(failed)
+        if me == mb:
+            return self.local.new_empty((m, 0)), 0, 0
+        r = 0 if failed is None else failed  # failed=None pivots on stream 0 (codec.py:49-51)
+        rows = [None if (j == r or t is None) else t[mb:me] for j, t in enumerate(self.rows)]
+        if out is None:
+            out = torch.empty((m, me - mb), dtype=torch.int64, device=self.local.device)
+        d, ovf = D.extract(rows, m, self.drv.params.l, r, wide=self.drv.params.w > 32, out=out,
+                           check_overflow=out.dtype == torch.int64)
+        if ovf:
+            raise OverflowError(f"{ovf} recovered values do not fit int64")
+        return d, mb, me
+
+    def close(self):
+        torch.cuda.current_stream(self.local.device).synchronize()
+        dist.barrier(group=self.drv.group)  # every read of every rank is done
+        self.rows = None
 
 
 @dataclass
@@ -233,13 +342,15 @@ class HaloSplit:
         halo = c_slice.new_zeros((m, H))
         if H and self.world > 1:
             ops = []
+            xh = _to_x(halo, self.group)
             if self.rank + 1 < self.world:
-                ops.append(dist.P2POp(dist.isend, c_slice[:, c_slice.shape[1] - H:].contiguous(),
-                                      self.rank + 1, self.group))
+                ops.append(dist.P2POp(dist.isend, _to_x(c_slice[:, c_slice.shape[1] - H:].contiguous(), self.group),
+                                      group=self.group, group_peer=self.rank + 1))
             if self.rank > 0:
-                ops.append(dist.P2POp(dist.irecv, halo, self.rank - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, xh, group=self.group, group_peer=self.rank - 1))
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+            halo = xh.to(c_slice.device)
         return torch.cat([halo, c_slice], dim=1).contiguous()
 
     def run(self, c_slice: torch.Tensor, g, failed: int | None = None):
@@ -255,14 +366,16 @@ class HaloSplit:
                                        y_begin=Hp, n_out=n_out, failed=failed)
 
     def gather(self, d_local: torch.Tensor, dst: int = 0):
-        sizes = torch.tensor([d_local.shape[1]], dtype=torch.int64)
+        xdev = torch.device("cpu") if _host_exchange(self.group) else d_local.device
+        sizes = torch.tensor([d_local.shape[1]], dtype=torch.int64, device=xdev)
         all_sizes = [torch.zeros_like(sizes) for _ in range(self.world)]
         dist.all_gather(all_sizes, sizes, group=self.group)
         maxw = int(max(s.item() for s in all_sizes))
         buf = d_local.new_zeros((d_local.shape[0], maxw))
         buf[:, : d_local.shape[1]] = d_local
+        buf = _to_x(buf, self.group)
         parts = [torch.empty_like(buf) for _ in range(self.world)] if self.rank == dst else None
-        dist.gather(buf, parts, dst=dst, group=self.group)
+        dist.gather(buf, parts, group=self.group, group_dst=dst)
         if self.rank != dst:
             return None
-        return torch.cat([p[:, : int(s.item())] for p, s in zip(parts, all_sizes)], dim=1)
+        return torch.cat([p[:, : int(s.item())] for p, s in zip(parts, all_sizes)], dim=1).to(d_local.device)

@@ -15,8 +15,9 @@ use, producing bit-identical results:
 One CTA owns all m streams of an output tile, so entanglement happens while
 the tile is staged into shared memory and extraction happens in registers:
 the entangled words never touch HBM.  ``failed=r`` recovers from the m-1
-other accumulators (worker r's result is computed and discarded, as a failed
-worker's would be); ``failed=None`` pivots on stream 0 and, with
+other accumulators and never reads stream r's (the tcgen05 kernel does not
+convolve stream r at all; the CUDA-core kernels compute it but the recovery
+never reads it); ``failed=None`` pivots on stream 0 and, with
 ``verify=True``, checks the redundant stream against the recovered outputs
 (a silent-data-corruption detector the entanglement gives for free).
 """
@@ -121,6 +122,30 @@ def plain_conv(block: StreamBlock, g, mode: str = "full", flavor: int | None = N
     return FusedResult(_finish(p, y, host), MAC_NAMES[flavor])
 
 
+def chain_operands(add, perm, n: int):
+    """The chain's ELEMENTWISE_ADD vector and PERMUTATION index map on the
+    device (either may be None), validated as the reference's LsbOp.validate /
+    Kernel.of_permutation do (ops.py:57-62, 84-112): the add vector has length
+    n or 1 (a length-1 vector is broadcast, ops.py:90), the permutation is a
+    bijection of [0, n) (checked by a device kernel) -- the chain kernels
+    index add[q] and perm[p] for every position, so anything shorter would
+    read out of bounds."""
+    add_dev = perm_dev = None
+    if add is not None:
+        add_dev = D.as_device(np.asarray(add, dtype=np.int64) if not isinstance(add, torch.Tensor) else add)
+        add_dev = add_dev.reshape(-1)
+        if add_dev.numel() == 1:
+            add_dev = add_dev.expand(n).contiguous()
+        elif add_dev.numel() != n:
+            raise ParameterError(f"kernel length {add_dev.numel()} != stream length {n}")
+    if perm is not None:
+        perm_dev = D.as_device(np.asarray(perm, dtype=np.int64) if not isinstance(perm, torch.Tensor) else perm)
+        if perm_dev.dim() != 1 or perm_dev.numel() != n:
+            raise ParameterError(f"permutation length {perm_dev.numel()} != stream length {n}")
+        D.perm_check(perm_dev)
+    return add_dev, perm_dev
+
+
 def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: int | None = None,
                          verify: bool = True, flavor: int | None = None, out_dtype=torch.int64
                          ) -> FusedResult:
@@ -135,9 +160,10 @@ def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: i
     p = block.params
     c, host = _prep(block)
     m, n = c.shape
-    add_dev = D.as_device(np.asarray(add, dtype=np.int64) if not isinstance(add, torch.Tensor) else add)
+    add_dev, perm_dev = chain_operands(add, perm, n)
+    if add_dev is None or perm_dev is None:
+        raise ParameterError("the cfg5 chain needs an add vector and a permutation")
     add_ent = D.shift_add(add_dev, add_dev, p.l)
-    perm_dev = D.as_device(np.asarray(perm, dtype=np.int64) if not isinstance(perm, torch.Tensor) else perm)
     g = np.asarray(g, dtype=np.int64)
     K = len(g)
     mc = D.host_max_abs(block.data) if host else D.max_abs(c)

@@ -16,7 +16,7 @@ rng = np.random.default_rng(5)
 n, K = 1 << 24, 256
 x = torch.from_numpy(rng.integers(-2048, 2048, (3, n), dtype=np.int64)).cuda().to(torch.int32)
 g = rng.integers(-2048, 2048, (K,), dtype=np.int64)
-p = nent.derive_params(3, 64)
+p = nent.derive_params(3, int(os.environ.get("NENT_W", "64")))
 fl = imma_flavor(D.signed_digits(2048 * ((1 << p.l) + 1)), D.signed_digits(2048))
 gd = D.taps_tensor(g, fl)
 L = n + K - 1

@@ -15,7 +15,7 @@ rng = np.random.default_rng(5)
 n, K = 1 << 24, 256
 x = torch.from_numpy(rng.integers(-2048, 2048, (3, n), dtype=np.int64)).cuda().to(torch.int32)
 g = rng.integers(-2048, 2048, (K,), dtype=np.int64)
-p = nent.derive_params(3, 64)
+p = nent.derive_params(3, 48 if "--w48" in sys.argv else 64)
 fl = imma_flavor(D.signed_digits(2048 * ((1 << p.l) + 1)), D.signed_digits(2048), mma_sync)
 gd = D.taps_tensor(g, fl)
 out = torch.empty((3, n + K - 1), dtype=torch.int32, device="cuda")

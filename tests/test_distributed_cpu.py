@@ -92,6 +92,45 @@ def _stream_worker(rank, world, port, cfg, failed_list, q):
         raise
 
 
+def _subgroup_worker(rank, world, port, q):
+    """StreamPerGPU and HaloSplit on a sub-group (global ranks 1..3 of 4):
+    peers and gather destinations are group-local ranks."""
+    try:
+        _init(rank, world, port)
+        from paper_1509_03838_b200 import workloads
+        from paper_1509_03838_b200.distributed import HaloSplit, StreamPerGPU, shard_bounds
+        sub = dist.new_group([1, 2, 3])
+        ok = True
+        if rank >= 1:
+            me = dist.get_rank(sub)
+            wl = workloads.make(1, n=500, K=17)
+            drv = StreamPerGPU(wl.params, group=sub, compute=OracleCompute())
+            c_own = torch.from_numpy(wl.c[me].copy())
+            from oracle import oracle as O
+            ref = O.full_conv(wl.c, wl.g)
+            for failed in (None, 0, 2):
+                out = drv.run(c_own, wl.g, failed=failed, dst=1)  # group rank 1 = global rank 2
+                if me == 1:
+                    ok = ok and np.array_equal(out.numpy(), ref)
+                else:
+                    ok = ok and out is None
+            wl2 = workloads.make(2, n=900, K=40)
+            b, e = shard_bounds(wl2.n, 3, me)
+            halo = HaloSplit(wl2.params, wl2.K, group=sub, compute=OracleCompute())
+            full = halo.gather(halo.run(torch.from_numpy(wl2.c[:, b:e].copy()), wl2.g, failed=1), dst=2)
+            if me == 2:
+                ok = ok and np.array_equal(full.numpy(), O.full_conv(wl2.c, wl2.g))
+        oks = [None] * world
+        dist.all_gather_object(oks, bool(ok))
+        if rank == 0:
+            q.put(all(oks))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        q.put(repr(exc))
+        raise
+
+
 def _halo_worker(rank, world, port, q):
     try:
         _init(rank, world, port)
@@ -138,6 +177,10 @@ def test_stream_per_gpu_every_failure(cfg, world):
 def test_stream_per_gpu_chain_cfg5_shape():
     # cfg5's chain (scale, add, permutation, conv) with M = 8 ranks
     assert _spawn(_stream_worker, 8, 5, [None, 3, 7]) is True
+
+
+def test_sub_group_peers_are_group_local():
+    assert _spawn(_subgroup_worker, 4) is True
 
 
 @pytest.mark.parametrize("world", [2, 3])

@@ -254,3 +254,26 @@ def test_admission_error():
     with pytest.raises(nent.AdmissionError):
         nent.run_pipeline(op, nent.StreamBlock(P3, np.full((3, 4), 1000)),
                           nent.FailureSpec(nent.Scheme.ENTANGLED))
+
+
+def test_inplace_int32_device_block_wide_words():
+    """An int32 device block cannot hold w=64 entangled words: the in-place
+    variants raise instead of keeping the low 32 bits (the copying variant and
+    int64 device blocks are exact)."""
+    p64 = nent.derive_params(3, 64)  # l = 21: eps = (c << 21) + c leaves int32
+    c = np.random.default_rng(3).integers(-(1 << 11), 1 << 11, (3, 512))
+    dev32 = torch.from_numpy(c).cuda().to(torch.int32)
+    with pytest.raises(nent.ParameterError):
+        nent.entangle_inplace(nent.StreamBlock(p64, dev32))
+    want = nent.entangle(nent.StreamBlock(p64, c)).data
+    b64 = nent.StreamBlock(p64, torch.from_numpy(c).cuda())
+    ent = nent.entangle_inplace(b64)
+    assert ent.data is b64.data and np.array_equal(ent.data.cpu().numpy(), want)
+    rec = nent.disentangle_inplace(ent, failed=1)
+    assert np.array_equal(rec.data.cpu().numpy(), c)
+    # small words fit an int32 buffer: in place stays allowed there
+    p32 = nent.derive_params(3, 32)
+    small = (c // 64).astype(np.int64)
+    b32 = nent.StreamBlock(p32, torch.from_numpy(small).cuda().to(torch.int32))
+    ent32 = nent.entangle_inplace(b32)
+    assert np.array_equal(ent32.data.cpu().numpy(), nent.entangle(nent.StreamBlock(p32, small)).data)

@@ -3,21 +3,25 @@
 
 Workload (BASELINE.json configs[1], the config the metric is quoted on):
 M=3 streams of N=2^24 int32 samples in [-2^11, 2^11-1], one 256-tap filter,
-geometry derive_params(3, 64) = (l=21, k=21); full linear convolution of every
-entangled stream, all 3 outputs recovered (failed=None pivots on stream 0 and
-checks the redundant stream).  One step = one launch of the fused
-entangle -> conv -> extract kernel over the whole batch, inputs resident in HBM.
-The kernel is the exact digit-sliced tensor-core convolution on the 5th-gen
-tensor cores (tcgen05.mma kind::i8, TMEM accumulators, warp-specialised): the
-35-bit entangled words become 5 int8 digit planes, the 12-bit taps 2.
+full linear convolution of every entangled stream, all 3 outputs recovered
+(failed=None pivots on stream 0 and checks the redundant stream).  One step =
+one launch of the fused entangle -> conv -> extract kernel over the whole
+batch, inputs resident in HBM.  The codec geometry is derive_params(3, 48) =
+(l=16, k=16) by default (--w 64 selects the (21, 21) geometry; the recovered
+outputs are identical): its 28-bit entangled words are 4
+int8 digit planes on the 5th-gen tensor cores (tcgen05.mma kind::i8, TMEM
+accumulators), the fused m = 3 kernel conv_tc05_m3.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                  [--w 48|64] [--config 2|3|5]
 
-N>1 (torchrun): halo-split weak scaling -- rank p owns a 2^24-sample slice of
-an N*2^24-sample signal; the K-1 = 255-sample halo comes from rank p-1 over
-NCCL once at setup; the timed region has no collective.  Rank 0 prints one
-JSON line.  --impl reference times the reference algorithm's CPU restatement
-(oracle/, all host threads) on the same workload; only rank 0 runs it.
+N>1 (torchrun): cfg2 halo-split weak scaling through distributed.HaloSplit --
+rank p owns a 2^24-sample slice; the halo comes from rank p-1 over NCCL once
+at setup; the timed region has no collective.  At N=4 and N=8 the
+stream-per-GPU configs (cfg3 on 4 GPUs, cfg5 on 8) are measured as well and
+attached as "stream_per_gpu"; --config 3|5 makes them the headline line.
+--impl reference times the reference algorithm's CPU restatement (oracle/,
+all host threads) on the same workload; only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -40,8 +44,8 @@ sys.path.insert(0, str(REPO))
 
 METRIC = "entangled int conv output samples/s; overhead vs non-entangled conv (%)"
 UNIT = "samples/s"
-WORKLOAD = "cfg2: M=3, N=2^24 int32 in [-2^11,2^11), K=256 taps, (m,w,l,k)=(3,64,21,21), full conv"
 B2B_ROUNDS = 3  # alternations of the back-to-back entangled / plain blocks (overhead headline)
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
 def parse():
@@ -50,6 +54,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--w", type=int, default=48, choices=[48, 64],
+                    help="codec word width of the cfg2 geometry: 48 -> (3,48,16,16), 64 -> (3,64,21,21)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+                    help="2: cfg2 (halo-split for N>1); 3/5: stream-per-GPU cfg3 (N=4) / cfg5 (N=8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the other-config section")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -64,6 +72,31 @@ def dist_env():
 
 def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a, dtype="<i8").tobytes()).hexdigest()
+
+
+def hbm_peak() -> tuple[float, str]:
+    """Measured HBM copy bandwidth (GB/s) of this pool's B200s."""
+    try:
+        v = float(json.loads((REPO / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload_name(w: int) -> str:
+    from paper_1509_03838_b200.params import derive_params
+    p = derive_params(3, w)
+    return (f"cfg2: M=3, N=2^24 int32 in [-2^11,2^11), K=256 taps, (m,w,l,k)=({p.m},{p.w},{p.l},{p.k}), "
+            "full conv, failed=None + redundant-stream check")
+
+
+def bench_config(world: int, w: int, cfg: int = 2) -> dict:
+    """The `config` object both arms print (identical dicts)."""
+    if cfg != 2:
+        return {"workload": f"cfg{cfg} stream-per-GPU", "parallelism": "stream-per-GPU", "n_ranks": world}
+    return {"workload": workload_name(w), "samples_per_step": 3 * ((1 << 24) * world + 255),
+            "parallelism": "halo-split" if world > 1 else "single GPU",
+            "l2": "inputs 201 MB + outputs 201 MB per GPU and step > 126 MB L2; no flush needed"}
 
 
 # ----------------------------------------------------------------- clocks --
@@ -134,17 +167,19 @@ class ClockSampler:
 
 # -------------------------------------------------------------- workload --
 
-def make_inputs(rank: int, n: int, K: int):
+def make_inputs(rank: int, n: int, K: int, w: int = 48):
     """Rank 0 holds the canonical cfg2 draw (seed 2); rank p > 0 draws its
     slice from seed (2, p) -- same shapes and value distribution."""
     from paper_1509_03838_b200 import workloads
+    from paper_1509_03838_b200.params import derive_params
 
     wl0 = workloads.make(2, n=n, K=K)  # the filter is drawn after the streams: full draw
+    p = derive_params(3, w)
     if rank == 0:
-        return wl0.params, wl0.c, wl0.g
+        return p, wl0.c, wl0.g
     rng = np.random.default_rng([2, rank])
     c = rng.integers(-(1 << 11), 1 << 11, (3, n), dtype=np.int64)
-    return wl0.params, c, wl0.g  # every rank uses the same filter
+    return p, c, wl0.g  # every rank uses the same filter
 
 
 def event_time(fn, stream, reps=1):
@@ -157,6 +192,16 @@ def event_time(fn, stream, reps=1):
     return a, b
 
 
+def timed_ms(fn, stream, reps: int) -> float:
+    """Average ms per call of `reps` back-to-back calls (CUDA events on `stream`)."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    a, b = event_time(fn, stream, reps)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
 # ------------------------------------------------------------ our device path --
 
 def run_ours(args):
@@ -165,8 +210,8 @@ def run_ours(args):
 
     from paper_1509_03838_b200 import _device as D
     from paper_1509_03838_b200 import fused
-    from paper_1509_03838_b200._lib import (BENCH_IMMA, BENCH_TC05, MAC_F64, MAC_G64, MAC_I32, MAC_NAMES, MAC_S64,
-                                            MAC_W64, imma_flavor, is_imma)
+    from paper_1509_03838_b200._lib import BENCH_IMMA, BENCH_TC05, MAC_F64, MAC_NAMES, imma_flavor
+    from paper_1509_03838_b200.distributed import HaloSplit
     from paper_1509_03838_b200.hostpath import ChunkedEntangledConv
 
     rank, world, local = dist_env()
@@ -185,36 +230,45 @@ def run_ours(args):
             dist.init_process_group(backend)
     xdev = dev if backend == "nccl" else torch.device("cpu")  # where collectives' tensors live
 
+    if args.config in (3, 5):  # stream-per-GPU as the headline line
+        res = run_stream_per_gpu(args.config, args.steps, args.warmup, dev, backend)
+        if rank == 0:
+            if res is None:
+                print(json.dumps({"metric": METRIC, "unavailable": f"cfg{args.config} needs WORLD_SIZE == "
+                                  f"{4 if args.config == 3 else 8} (one stream per GPU), got {world}"}))
+            else:
+                print(json.dumps({"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+                                  "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                                  "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                                  "overhead_pct": res["overhead_pct"], "dtype": "int32 in/out, exact int64",
+                                  "data": "synthetic (canonical seeded draw, SURVEY.md 8d)",
+                                  "config": bench_config(world, args.w, args.config), "stream_per_gpu": res,
+                                  "gpu_launches": None}))
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
     n, K = 1 << 24, 256
-    params, c_np, g = make_inputs(rank, n, K)
+    params, c_np, g = make_inputs(rank, n, K, args.w)
     m, H = params.m, K - 1
     c_dev = torch.from_numpy(c_np).to(dev).to(torch.int32)
-    if world > 1:  # halo-split: the samples left of this rank's slice come from rank-1
-        Hp = (H + 3) // 4 * 4  # K-1 rounded up to 4 words: the kernel's tiles then start 16-byte aligned
-        halo = torch.zeros((m, Hp), dtype=torch.int32, device=xdev)
-        ops = []
-        if rank + 1 < world:
-            ops.append(dist.P2POp(dist.isend, c_dev[:, n - Hp:].contiguous().to(xdev), rank + 1))
-        if rank > 0:
-            ops.append(dist.P2POp(dist.irecv, halo, rank - 1))
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        x_dev = torch.cat([halo.to(dev), c_dev], dim=1).contiguous()
-        n_out = n + (H if rank == world - 1 else 0)  # the last rank also owns the K-1 tail
-        period, n_in, y_begin = Hp + n + H, Hp + n, Hp  # rank 0 keeps a zero halo (left edge)
+    if world > 1:  # halo-split: [halo | slice] from rank-1, once, outside the timed region
+        halo_drv = HaloSplit(params, K)
+        x_dev = halo_drv.exchange_halo(c_dev)
+        win = halo_drv.window(n)
     else:
         x_dev = c_dev
-        n_out, period, n_in, y_begin = n + H, n + H, n, 0
+        win = {"period": n + H, "n_in": n, "y_begin": 0, "n_out": n + H}
+    n_out, period, n_in, y_begin = win["n_out"], win["period"], win["n_in"], win["y_begin"]
 
     max_c = 1 << 11
     eps_bound = max_c * ((1 << params.l) + 1)
-    flavor = fused.conv_flavor(eps_bound, g, n_out=n_out)             # imma5x2 for cfg2
+    flavor = fused.conv_flavor(eps_bound, g, n_out=n_out)             # imma4x2 (w=48) / imma5x2 (w=64)
     core_flavor = fused.conv_flavor(eps_bound, g, allow_imma=False)   # f64: the CUDA-core path
     plain_same = flavor                                               # same kernel, same digits
     plain_fast = fused.conv_flavor(max_c, g, n_out=n_out)             # fastest plain: imma2x2
     plain_core = fused.conv_flavor(max_c, g, allow_imma=False)        # i32
     taps = {f: D.taps_tensor(g, f) for f in {flavor, core_flavor, plain_same, plain_fast, plain_core}}
-    # IMMA: digit-split Toeplitz tap tables prepared once (the taps are fixed)
     tables = {f: D.imma_table(taps[f], K, f, y_begin) for f in taps}
     # output rows at 128-byte aligned starts (a padded row pitch; the kernels take
     # one pointer per row), so every warp's 128-byte store is one whole line
@@ -226,8 +280,7 @@ def run_ours(args):
 
     def fused_step(fl=flavor):
         D.fused_conv(x_dev, taps[fl], K, params.l, fl, None, params.w > 32, period, n_in=n_in,
-                     y_begin=y_begin, n_out=n_out, out=d_dev, mismatch=mismatch,
-                     imma_table=tables[fl])
+                     y_begin=y_begin, n_out=n_out, out=d_dev, mismatch=mismatch, imma_table=tables[fl])
 
     def failed_step(r=1, fl=flavor):  # one stream lost: recovery from the two survivors
         D.fused_conv(x_dev, taps[fl], K, params.l, fl, r, params.w > 32, period, n_in=n_in,
@@ -242,9 +295,11 @@ def run_ours(args):
         plain(plain_same)
         plain(plain_fast)
     torch.cuda.synchronize(dev)
+    fused_step()
+    kernel_kind = D.last_conv_kernel()
+    torch.cuda.synchronize(dev)
 
     exact = None
-    known = None
     if rank == 0 and world == 1:  # parity of the benchmarked output itself
         known = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())["cfg2"]["d"]
         exact = sha(d_dev.to(torch.int64).cpu().numpy()) == known and int(mismatch.item()) == 0
@@ -267,33 +322,24 @@ def run_ours(args):
     if world > 1:  # parity of every shard against one single-GPU run over the whole signal
         exact = check_shards(D, d_dev, rank, world, n, K, params, g, flavor, dev, xdev)
 
-    # ---------------- the plain convolutions timed like `value` ----------------
+    # ---------------- overhead: the plain convolutions timed like `value` ----------------
     # K back-to-back launches each on the same stream, CUDA events around them
-    # (the same protocol as the timed region above), the three blocks alternated
-    # B2B_ROUNDS times and each candidate's median taken, so the entangled and
-    # the plain blocks see the same box state (one plain block alone varied
-    # 0.117-0.136 ms between boxes while the entangled one stayed at 0.146-0.149)
+    # (the protocol of the timed region), the blocks alternated B2B_ROUNDS
+    # times and each candidate's median taken, so every leg sees the same box state
     rounds = {"entangled": [], "plain_same_kernel": [], "plain_fastest": []}
     blocks = (("entangled", fused_step), ("plain_same_kernel", lambda: plain(plain_same)),
               ("plain_fastest", lambda: plain(plain_fast)))
     for _ in range(B2B_ROUNDS):
         for name, fn in blocks:
-            fn()
-            torch.cuda.synchronize(dev)
-            a0, a1 = event_time(fn, stream, args.steps)
-            torch.cuda.synchronize(dev)
-            rounds[name].append(a0.elapsed_time(a1) / args.steps)
+            rounds[name].append(timed_ms(fn, stream, args.steps))
     b2b = {k: float(np.median(v)) for k, v in rounds.items()}
-
-    # ---------------- interleaved comparisons (per-launch CUDA events) ----------------
     cands = {
         "entangled": lambda: fused_step(flavor),
-        "entangled_cuda_core": lambda: fused_step(core_flavor),
         "entangled_failed_r1": lambda: failed_step(1),
         "plain_same_kernel": lambda: plain(plain_same),
         "plain_fastest": lambda: plain(plain_fast),
+        "entangled_cuda_core": lambda: fused_step(core_flavor),
         "plain_cuda_core_same_width": lambda: plain(core_flavor),
-        "plain_cuda_core_narrowest": lambda: plain(plain_core),
     }
     evs = {k: [] for k in cands}
     for _ in range(max(5, min(args.steps, 11))):
@@ -306,9 +352,21 @@ def run_ours(args):
     def ovh(a, b):
         return statistics.median([(x - y) / y * 100 for x, y in zip(t[a], t[b])])
 
+    overhead_pct = (b2b["entangled"] - b2b["plain_same_kernel"]) / b2b["plain_same_kernel"] * 100
+    overhead = {
+        "back_to_back_ms": b2b,
+        "interleaved_vs_plain_same_kernel_pct": ovh("entangled", "plain_same_kernel"),
+        "vs_plain_fastest_pct": (b2b["entangled"] - b2b["plain_fastest"]) / b2b["plain_fastest"] * 100,
+        "failed_r1_vs_plain_same_kernel_pct": ovh("entangled_failed_r1", "plain_same_kernel"),
+        "cuda_core_same_width_pct": ovh("entangled_cuda_core", "plain_cuda_core_same_width"),
+        "interleaved_ms": med,
+        "flavors": {"entangled": MAC_NAMES[flavor], "plain_same_kernel": MAC_NAMES[plain_same],
+                    "plain_fastest": MAC_NAMES[plain_fast], "cuda_core": MAC_NAMES[core_flavor]},
+    }
+
     # ---------------- measured pipe peaks (roofline denominators) ----------------
     peaks = {}
-    for kind in (BENCH_TC05, BENCH_IMMA, MAC_F64, MAC_I32, MAC_W64, MAC_S64, MAC_G64):
+    for kind in (BENCH_TC05, BENCH_IMMA, MAC_F64):
         grid = 148 if kind == BENCH_TC05 else 148 * 8
         iters = {BENCH_TC05: 2000, BENCH_IMMA: 1024}.get(kind, 4096)
         D.microbench(kind, grid, 256, 64)
@@ -323,33 +381,93 @@ def run_ours(args):
         peaks[MAC_NAMES[kind]] = best
     np_, ng = (flavor >> 8) & 15, (flavor >> 12) & 15
     # the dominant kernel's average launch duration over the timed region (one
-    # fused launch per step, back to back on `stream`); the interleaved
-    # per-launch median is reported beside it
+    # fused launch per step, back to back on `stream`)
     kern_ms = ms_step
     macs_alg = m * n * K                      # M*N*K
     digit_macs = macs_alg * np_ * ng          # int8 digit products the method needs
     achieved = 2 * digit_macs / (kern_ms / 1e3) / 1e12
-    kernel_kind = D.imma_kernel(flavor, K, m, True)
-    peak_key = "tcgen05_i8" if kernel_kind == "tcgen05" else "imma_s8_mma_sync"
-    peak = 2 * peaks[peak_key] / 1e12
+    tc = kernel_kind.startswith("tcgen05")
+    peak = 2 * peaks["tcgen05_i8" if tc else "imma_s8_mma_sync"] / 1e12
     kt = (K + 127 + 127) // 128 * 128      # tcgen05 Toeplitz band: K + 127 padded to 128
-    issued_macs = m * (n + K - 1) * kt * np_ * ng if kernel_kind == "tcgen05" else None
+    issued_macs = m * (n + K - 1) * kt * np_ * ng if tc else None
+    hbm, hbm_src = hbm_peak()
+    io_bytes = m * (n_in + n_out) * 4  # int32 streams in, int32 recovered outputs out
     traffic = None
     tf = REPO / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(MAC_NAMES[flavor], {}).get("bytes_per_launch")
+            traffic = json.loads(tf.read_text()).get(kernel_kind, {}).get("bytes_per_launch")
         except Exception:
             traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": kernel_kind, "flavor": MAC_NAMES[flavor],
+                "algorithmic_per_launch": {"conv_macs": macs_alg, "digit_planes": np_, "tap_digits": ng,
+                                           "digit_macs": digit_macs, "tensor_macs_issued": issued_macs,
+                                           "hbm_bytes": io_bytes},
+                "issued_frac": (2 * issued_macs / (kern_ms / 1e3) / 1e12 / peak) if issued_macs else None,
+                "hbm_gb_s": io_bytes / (kern_ms / 1e3) / 1e9, "hbm_frac": io_bytes / (kern_ms / 1e3) / 1e9 / hbm,
+                "hbm_peak_gb_s": hbm, "hbm_peak_source": hbm_src,
+                "peak_source": "measured in this run: nent_microbench tcgen05.mma kind::i8 128x128x32 chains, "
+                               "1 CTA/SM" if tc else "measured in this run: mma.sync s8 microbench",
+                "peaks_measured_gmac_s": {k: v / 1e9 for k, v in peaks.items()}}
 
     # ---------------- e2e through the host-buffer path ----------------
-    # Every rank pushes its own host-resident input ([halo | slice] for N > 1)
-    # through the pipeline; the job time is the max over ranks.
-    e2e = None
-    if world == 1:
-        xin_np = c_np.astype(np.int32)
-    else:
-        xin_np = x_dev.cpu().numpy()  # this rank's staged [halo | slice] words
+    e2e = run_e2e(params, g, flavor, x_dev, d_dev, c_np, world, rank, y_begin, n_out, samples_job, dev, xdev)
+    api = run_api_e2e(params, c_np, g, dev) if (rank == 0 and world == 1 and not args.no_extras) else None
+
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = other_configs(D, fused, dev, stream, args.w)
+        extras["codec_passes"] = codec_passes(D, dev, stream, params, c_dev, g)
+        extras["geometry_ab"] = geometry_ab(D, dev, stream, c_dev, g, args.w)
+    spg = None
+    if world in (4, 8) and not args.no_extras:
+        del d_dev, y_plain
+        torch.cuda.empty_cache()
+        spg = run_stream_per_gpu(3 if world == 4 else 5, min(args.steps, 20), args.warmup, dev, backend)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(c_np, g, params, args.cpu_seconds)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "overhead_pct": overhead_pct,
+            "exact": exact, "mismatches": int(mismatch.item()),
+            "dtype": "int8 digits x int8 digits -> int32 -> int64 (exact integer; int32 in/out)",
+            "data": "synthetic (canonical seeded cfg2 draw, SURVEY.md 8d)",
+            "config": bench_config(world, args.w),
+            "overhead": overhead,
+            "roofline": roofline,
+            "e2e": e2e,
+            "e2e_numpy_api": api,
+            "gpu_launches": args.steps,  # one fused kernel per step (tap table prepared before)
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "stream_per_gpu": spg,
+            "other_configs": extras,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(params, g, flavor, x_dev, d_dev, c_np, world, rank, y_begin, n_out, samples_job, dev, xdev):
+    """The same metric end to end through the public host-buffer API
+    (hostpath.ChunkedEntangledConv): pinned int32 host input -> H2D -> fused
+    kernel -> D2H of the recovered int32 outputs, every step; `reps` steps
+    streamed as one CUDA graph, wall clock incl. sync, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_03838_b200.hostpath import ChunkedEntangledConv
+
+    m, H = params.m, len(g) - 1
+    xin_np = c_np.astype(np.int32) if world == 1 else x_dev.cpu().numpy()  # [halo | slice] for N > 1
     n_e = xin_np.shape[1]
     pipe = ChunkedEntangledConv(params, n_e, g, flavor)  # 2^20-sample chunks, output lag 1
     c_host = torch.from_numpy(xin_np).pin_memory()
@@ -359,21 +477,19 @@ def run_ours(args):
     def shard_ok() -> bool:
         return bool(torch.equal(d_host[:, o0:o0 + n_out], d_dev.cpu()))
 
-    pipe.capture(c_host, d_host)  # the whole multi-stream job as one CUDA graph
+    reps = 8
+    pipe.capture(c_host, d_host)
     d_host.zero_()
     pipe.replay()
     torch.cuda.synchronize(dev)
     ok = shard_ok()
-    reps = max(3, min(args.steps, 8))
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(reps):
+    for _ in range(3):
         pipe.replay()
         torch.cuda.synchronize(dev)
-    single_s = (time.perf_counter() - t0) / reps
-    # streaming: `reps` steps as one continuous pipeline (each step still
-    # copies all its inputs in and all its outputs out; fill/drain once)
+    single_s = (time.perf_counter() - t0) / 3
     pipe.capture(c_host, d_host, jobs=reps)
     d_host.zero_()
     pipe.replay()
@@ -389,109 +505,92 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s, single_s, bad = (float(v) for v in tt.tolist())
-    if exact is not None:
-        exact = exact and bad == 0.0
-    e2e = {"value": samples_job / e2e_s, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes() * world,
-           "d2h_bytes_per_step": pipe.d2h_bytes() * world, "ms_per_step": e2e_s * 1e3,
-           "steps_streamed": reps, "single_step_ms": single_s * 1e3, "bit_exact_vs_device_output": bad == 0.0,
-           "path": "ChunkedEntangledConv on every rank: pinned int32 host -> 3-stage pipeline (H2D stream / "
-                   "fused-kernel stream / D2H stream, 2^20-sample chunks each moved as one 2-D DMA "
-                   "per direction, D2H lagging H2D by one chunk, 4-buffer ring, 256-byte-aligned "
-                   "host transfers), "
-                   "the steps captured as one continuous CUDA graph (a stream of batches: the next "
-                   "step's input copies overlap the previous step's last output copies); wall clock "
-                   "over all steps incl. sync, max over ranks; single_step_ms = one step per graph "
-                   "replay + sync" + ("; N > 1: each rank's host input is its [halo | slice]" if world > 1 else ""),
-           "pcie_floor_ms": "~4.0 per GPU (201 MB each way at the ~50 GB/s measured concurrently)",
-           "kernels_per_step": pipe.launches // reps}
+    return {"value": samples_job / e2e_s, "unit": UNIT, "h2d_bytes_per_step": pipe.h2d_bytes() * world,
+            "d2h_bytes_per_step": pipe.d2h_bytes() * world, "ms_per_step": e2e_s * 1e3,
+            "steps_streamed": reps, "single_step_ms": single_s * 1e3, "bit_exact_vs_device_output": bad == 0.0,
+            "path": "hostpath.ChunkedEntangledConv: pinned int32 host -> chunked H2D / fused kernel / D2H "
+                    "on 3 streams, steps captured as one CUDA graph (DESIGN.md 7)",
+            "kernels_per_step": pipe.launches // reps}
 
-    extras = None
-    if rank == 0 and world == 1 and not args.no_extras:
-        extras = other_configs(D, fused, dev, stream)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(c_np, g, params, args.cpu_seconds)
+def run_api_e2e(params, c_np, g, dev):
+    """The drop-in call a reference user makes, timed end to end:
+    fused.entangled_conv(StreamBlock(params, int64 numpy)) -> int64 numpy
+    (pageable copies both ways, flavour chosen from the data's bound)."""
+    import torch
 
-    if rank == 0:
-        out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": "int8 digits x int8 digits -> int32 -> int64 (exact integer; int32 in/out)",
-            "data": "synthetic (canonical seeded cfg2 draw, SURVEY.md 8d)",
-            "config": {"workload": WORKLOAD, "samples_per_step": samples_job,
-                       "parallelism": "halo-split" if world > 1 else "single GPU",
-                       "l2": "inputs 201 MB + outputs 201 MB per step > 126 MB L2; no flush needed",
-                       "mac_flavor": MAC_NAMES[flavor], "failed": None, "verify_redundant_stream": True},
-            "overhead_pct": (b2b["entangled"] - b2b["plain_same_kernel"]) / b2b["plain_same_kernel"] * 100,
-            "overhead": {
-                "headline": "back-to-back: K launches of the fused entangled kernel vs K launches of the "
-                            "same kernel and digit geometry on the plain streams, the blocks alternated "
-                            f"{B2B_ROUNDS} times, median per candidate",
-                "back_to_back_ms": b2b, "back_to_back_rounds_ms": rounds,
-                "back_to_back_vs_plain_fastest_pct": (b2b["entangled"] - b2b["plain_fastest"])
-                                                     / b2b["plain_fastest"] * 100,
-                "interleaved_vs_plain_same_kernel_pct": ovh("entangled", "plain_same_kernel"),
-                "vs_plain_same_kernel_pct": ovh("entangled", "plain_same_kernel"),
-                "vs_plain_fastest_pct": ovh("entangled", "plain_fastest"),
-                "cuda_core_entangled_vs_plain_same_width_pct": ovh("entangled_cuda_core",
-                                                                   "plain_cuda_core_same_width"),
-                "vs_plain_cuda_core_narrowest_pct": ovh("entangled", "plain_cuda_core_narrowest"),
-                "flavors": {"entangled": MAC_NAMES[flavor], "entangled_cuda_core": MAC_NAMES[core_flavor],
-                            "plain_same_kernel": MAC_NAMES[plain_same], "plain_fastest": MAC_NAMES[plain_fast],
-                            "plain_cuda_core_narrowest": MAC_NAMES[plain_core]},
-                "ms": med,
-                "note": "plain_same_kernel runs the identical kernel/digit geometry on the plain streams "
-                        "(isolates entangle+extract); plain_fastest uses the digits the 12-bit plain "
-                        "samples need (2 planes instead of the entangled words' 5); entangled_failed_r1 "
-                        "loses stream 1: the two survivors are convolved and all three outputs recovered "
-                        "(the lost stream is never computed)"},
-            "roofline": {"bound": "tensor",
-                         "pipe": ("tcgen05.mma kind::i8 (5th-gen tensor cores, TMEM accumulators)"
-                                  if kernel_kind == "tcgen05" else "IMMA (mma.sync m16n8k32 s8)"),
-                         "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                         "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": (f"nent::tcc::conv_tc05_kernel<true,{np_},{kt // 32}> ({MAC_NAMES[flavor]})"
-                                    if kernel_kind == "tcgen05"
-                                    else f"nent::conv_imma_kernel<3,{ng},true> ({MAC_NAMES[flavor]})"),
-                         "algorithmic_per_launch": {"conv_macs": macs_alg, "digit_macs": digit_macs,
-                                                    "digit_planes": np_, "tap_digits": ng,
-                                                    "tensor_macs_issued": issued_macs,
-                                                    "note": "achieved counts the method's digit MACs "
-                                                            "(M*N*K*np*ng); the tcgen05 Toeplitz band "
-                                                            "issues KT/K more (zero taps outside the band)"},
-                         "issued_tops": (2 * issued_macs / (kern_ms / 1e3) / 1e12) if issued_macs else None,
-                         "launch_ms": {"timed_region_avg": kern_ms, "interleaved_median": med["entangled"]},
-                         "peak_source": (f"measured in this run: nent_microbench {peak_key} "
-                                         + ("(tcgen05.mma 128x128x32 chains, 1 CTA/SM)" if kernel_kind == "tcgen05"
-                                            else "(16 independent accumulators per warp, 148*8 CTAs x 8 warps)")),
-                         "cuda_core_path": {"flavor": MAC_NAMES[core_flavor],
-                                            "achieved_tflops": 2 * macs_alg / (med["entangled_cuda_core"] / 1e3) / 1e12,
-                                            "peak_tflops": 2 * peaks[MAC_NAMES[core_flavor]] / 1e12},
-                         "peaks_measured_gmac_s": {k: v / 1e9 for k, v in peaks.items()},
-                         # BASELINE.json north_star's roofline: the 64-bit integer multiply rate
-                         # of the CUDA cores (measured here: IMAD.WIDE and generic 64-bit MAC
-                         # chains); the fused kernel's exact int64 conv MACs (M*N*K) per second
-                         # against it
-                         "int64_cuda_core_roofline": {
-                             "conv_macs_per_s": macs_alg / (kern_ms / 1e3),
-                             "peak_w64_macs_per_s": peaks["w64"], "peak_g64_macs_per_s": peaks["g64"],
-                             "frac_vs_w64": macs_alg / (kern_ms / 1e3) / peaks["w64"],
-                             "frac_vs_g64": macs_alg / (kern_ms / 1e3) / peaks["g64"],
-                             "note": "the tensor-core digit slicing delivers exact 64-bit convolution "
-                                     "MACs faster than the CUDA cores can issue 64-bit multiplies"}},
-            "e2e": e2e,
-            "gpu_launches": args.steps,  # one fused kernel per step (tap table prepared before)
-            "exact": exact,
-            "mismatches": int(mismatch.item()),
-            "clocks": clocks.summary(),
-            "other_configs": extras,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(out))
-    if world > 1:
-        dist.destroy_process_group()
+    import paper_1509_03838_b200 as nent
+    from paper_1509_03838_b200 import fused
+
+    block = nent.StreamBlock(params, c_np)
+    res = fused.entangled_conv(block, g)  # warm-up
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        res = fused.entangled_conv(block, g)
+        ts.append(time.perf_counter() - t0)
+    known = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())["cfg2"]["d"]
+    s = min(ts)
+    samples = res.outputs.data.size
+    return {"value": samples / s, "unit": UNIT, "ms_per_call": s * 1e3,
+            "h2d_bytes_per_step": int(c_np.nbytes), "d2h_bytes_per_step": int(res.outputs.data.nbytes),
+            "exact": sha(res.outputs.data) == known and res.mismatches == 0,
+            "call": "fused.entangled_conv(StreamBlock(params, numpy int64 (3, 2^24)), g) -> numpy int64",
+            "flavor": res.flavor}
+
+
+def codec_passes(D, dev, stream, params, c_dev, g):
+    """K1 (entangle) and K3 (extract) alone on cfg2-sized streams, against the
+    HBM roofline: bytes moved per launch / launch time."""
+    import torch
+
+    hbm, _ = hbm_peak()
+    m, n = c_dev.shape
+    res = {}
+    eps = torch.empty((m, n), dtype=torch.int32, device=dev)
+    ms = timed_ms(lambda: D.entangle(c_dev, params.l, out_dtype=torch.int32, out=eps), stream, 20)
+    byts = m * n * 4 * 2  # read c (each sample once from HBM; c_{i-1} hits L2), write eps
+    res["entangle_k1"] = {"ms": ms, "gb_s": byts / (ms / 1e3) / 1e9, "hbm_frac": byts / (ms / 1e3) / 1e9 / hbm,
+                          "bytes": byts, "shape": "3 x 2^24 int32 -> int32"}
+    delta = torch.empty((m, n), dtype=torch.int64, device=dev)
+    delta.copy_(eps)  # any consistent words do: the pass's cost does not depend on the values
+    out = torch.empty((m, n), dtype=torch.int32, device=dev)
+    for r in (0, 1):
+        ms = timed_ms(lambda: D.extract(delta, m, params.l, r, wide=params.w > 32, out=out,
+                                        check_overflow=False), stream, 20)
+        byts = (m - 1) * n * 8 + m * n * 4
+        res[f"extract_k3_r{r}"] = {"ms": ms, "gb_s": byts / (ms / 1e3) / 1e9,
+                                   "hbm_frac": byts / (ms / 1e3) / 1e9 / hbm, "bytes": byts,
+                                   "shape": "2 surviving int64 rows of 2^24 -> 3 int32 rows"}
+    return res
+
+
+def geometry_ab(D, dev, stream, c_dev, g, w):
+    """The cfg2 fused kernel at the other codec geometry (same recovered
+    outputs; 5 digit planes at w=64 vs 4 at w=48)."""
+    import torch
+
+    import paper_1509_03838_b200 as nent
+    from paper_1509_03838_b200._lib import MAC_NAMES, imma_flavor
+
+    other = 64 if w == 48 else 48
+    p = nent.derive_params(3, other)
+    m, n = c_dev.shape
+    K = len(g)
+    fl = imma_flavor(D.signed_digits(2048 * ((1 << p.l) + 1)), D.signed_digits(int(np.abs(g).max())))
+    gd = D.taps_tensor(g, fl)
+    tab = D.imma_table(gd, K, fl, 0)
+    L = n + K - 1
+    out = torch.empty((m, (L + 31) // 32 * 32), dtype=torch.int32, device=dev)[:, :L]
+    mm = torch.zeros(1, dtype=torch.int64, device=dev)
+    f = lambda: D.fused_conv(c_dev, gd, K, p.l, fl, None, True, L, n_in=n, out=out, mismatch=mm,  # noqa: E731
+                             imma_table=tab)
+    ms = timed_ms(f, stream, 20)
+    kern = D.last_conv_kernel()
+    known = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())["cfg2"]["d"]
+    ok = sha(out.to(torch.int64).cpu().numpy()) == known and int(mm.item()) == 0
+    return {"geometry": f"({p.m},{p.w},{p.l},{p.k})", "flavor": MAC_NAMES[fl], "kernel": kern, "ms": ms,
+            "samples_per_s": m * L / (ms / 1e3), "exact": ok}
 
 
 def check_shards(D, d_dev, rank, world, n, K, params, g, flavor, dev, xdev):
@@ -532,14 +631,17 @@ def check_shards(D, d_dev, rank, world, n, K, params, g, flavor, dev, xdev):
     return ok
 
 
-def other_configs(D, fused, dev, stream):
-    """The other BASELINE configs through the same fused path: ms per launch,
-    output samples/s, and the known-answer digest check (no failure)."""
+
+def other_configs(D, fused, dev, stream, w):
+    """The other BASELINE configs through the same fused path on one GPU:
+    ms per launch, output samples/s, and the known-answer digest check (no
+    failure); cfg4 inner and outer products against the HBM roofline."""
     import torch
 
     from paper_1509_03838_b200 import workloads
-    from paper_1509_03838_b200._lib import MAC_NAMES
+    from paper_1509_03838_b200._lib import MAC_G64, MAC_NAMES
 
+    hbm, hbm_src = hbm_peak()
     digests = json.loads((REPO / "tests" / "golden" / "digests.json").read_text())
     res = {}
     for cfg in (1, 3, 5):
@@ -562,8 +664,6 @@ def other_configs(D, fused, dev, stream):
         fl = fused.conv_flavor(xb, wl.g, n_out=L)
         gd = D.taps_tensor(wl.g, fl)
         tab = D.imma_table(gd, K, fl, 0)
-        # m > 3 chain: tcgen05 conv of the chain rows + verifying extract (the
-        # route fused.entangled_chain_conv takes), else the fused kernel
         split = (chain and D.imma_kernel(fl, K, wl.m, True) != "tcgen05"
                  and D.imma_kernel(fl, K, wl.m, False) == "tcgen05")
         if split:
@@ -571,7 +671,6 @@ def other_configs(D, fused, dev, stream):
 
         def run():
             if chain:
-                # chain words in the coalesced interleave pass, then one record gather
                 D.interleave_chain(c, p.l, wl.scale, add, out=ct)
                 D.gather_records(ct, perm, out=xg)
                 if split:
@@ -587,35 +686,63 @@ def other_configs(D, fused, dev, stream):
         for _ in range(3):
             run()
         torch.cuda.synchronize(dev)
+        kern = D.last_conv_kernel()
         ok = sha(out.to(torch.int64).cpu().numpy()) == digests[f"cfg{cfg}"]["d"] and int(mm.item()) == 0
-        reps = 20 if cfg == 1 else 5
-        a, b = event_time(run, stream, reps)
-        torch.cuda.synchronize(dev)
-        ms = a.elapsed_time(b) / reps
-        res[f"cfg{cfg}"] = {"flavor": MAC_NAMES[fl], "ms": ms,
-                            "kernel": (("tcgen05 conv + verifying extract" if split else D.imma_kernel(fl, K, wl.m, True))
-                                       if (fl & 0xFF) == 7 else "cuda-core"), "samples_per_s": wl.m * L / (ms / 1e3),
-                            "conv_gmac_s": wl.m * n * K / (ms / 1e3) / 1e9, "exact": ok}
+        ms = timed_ms(run, stream, 20 if cfg == 1 else 5)
+        res[f"cfg{cfg}"] = {"flavor": MAC_NAMES[fl], "ms": ms, "kernel": ("tcgen05 conv + verifying extract"
+                                                                          if split else kern),
+                            "samples_per_s": wl.m * L / (ms / 1e3), "conv_gmac_s": wl.m * n * K / (ms / 1e3) / 1e9,
+                            "exact": ok}
+        if chain:  # per-pass breakdown of the chain (bytes moved / time)
+            passes = {"interleave_chain": (lambda: D.interleave_chain(c, p.l, wl.scale, add, out=ct),
+                                           2 * wl.m * n * 4 + n * 8),
+                      "gather_records": (lambda: D.gather_records(ct, perm, out=xg), 2 * wl.m * n * 4 + n * 4)}
+            if split:
+                passes["conv"] = (lambda: D.conv(xg, gd, K, fl, period=L, n_out=L, out=delta), 2 * wl.m * n * 4)
+                passes["extract_verify"] = (lambda: D.extract_verify(delta, wl.m, p.l, 0, p.w > 32, mm, out=out),
+                                            2 * wl.m * L * 4)
+            else:
+                passes["fused_conv_extract"] = (lambda: D.fused_conv(xg, gd, K, p.l, fl, None, True, L, n_in=n,
+                                                                     out=out, mismatch=mm, pre_entangled=True,
+                                                                     imma_table=tab), 2 * wl.m * n * 4)
+            res[f"cfg{cfg}"]["passes"] = {}
+            for name, (fn, byts) in passes.items():
+                pms = timed_ms(fn, stream, 5)
+                res[f"cfg{cfg}"]["passes"][name] = {"ms": pms, "bytes": byts, "gb_s": byts / (pms / 1e3) / 1e9,
+                                                    "hbm_frac": byts / (pms / 1e3) / 1e9 / hbm}
+        del c, out
+        torch.cuda.empty_cache()
     # cfg4 inner products (65,536 x 4,096 per stream, 3 streams)
     wl = workloads.make(4)
     c = torch.from_numpy(wl.c).to(dev).to(torch.int32)
     r = fused.entangled_inner(wl.params, c, wl.g)  # public API once: digest + redundant check
     ok = sha(r.outputs.data.to(torch.int64).cpu().numpy()) == digests["cfg4_inner"]["d"] and r.mismatches == 0
-    from paper_1509_03838_b200._lib import MAC_G64
     gd = D.taps_tensor(wl.g, MAC_G64)
-    outd = torch.empty((3, c.shape[1]), dtype=torch.int64, device=dev)
 
     def inner():
         D.fused_inner(c, gd, wl.params.l, None, True, MAC_G64, out_dtype=torch.int64)
 
-    inner()
-    a, b = event_time(inner, stream, 5)
-    torch.cuda.synchronize(dev)
-    ms = a.elapsed_time(b) / 5
+    ms = timed_ms(inner, stream, 5)
     res["cfg4_inner"] = {"flavor": r.flavor, "ms": ms, "hbm_gb_s": c.numel() * 4 / (ms / 1e3) / 1e9,
-                         "hbm_frac_of_measured": c.numel() * 4 / (ms / 1e3) / 1e9 / 6540.5, "exact": ok}
-    del outd
-    del c
+                         "hbm_frac": c.numel() * 4 / (ms / 1e3) / 1e9 / hbm, "hbm_peak_source": hbm_src,
+                         "exact": ok}
+    # cfg4 outer products: d[i, b, u, v] = c[i, b, u] g[v] recovered through the
+    # entangled domain; 3.3e12 outputs for the whole batch (26 TB as int64), so
+    # a window of B vectors is materialised (int32) into one reused buffer and
+    # timed against the HBM store roofline; the full batch is extrapolated
+    B = 16
+    n4 = wl.c.shape[2]
+    outo = torch.empty((3, B, n4, n4), dtype=torch.int32, device=dev)
+    cw = c[:, :B].contiguous()
+    ms = timed_ms(lambda: fused.entangled_outer(wl.params, cw, wl.g, out=outo), stream, 3)
+    ref = wl.c[:, :2, :, None] * wl.g[None, None, None, :]  # vectors 0 and 1 elementwise
+    ok = bool(np.array_equal(outo[:, :2].to(torch.int64).cpu().numpy(), ref))
+    store = outo.numel() * 4
+    res["cfg4_outer"] = {"vectors_timed": B, "ms": ms, "outputs_per_s": outo.numel() / (ms / 1e3),
+                         "store_gb_s": store / (ms / 1e3) / 1e9, "hbm_frac": store / (ms / 1e3) / 1e9 / hbm,
+                         "full_batch_s_extrapolated": ms / 1e3 * wl.c.shape[1] / B,
+                         "exact_vectors_0_1": ok, "out_dtype": "int32"}
+    del c, cw, outo
     torch.cuda.empty_cache()
     return res
 
@@ -815,13 +942,70 @@ def cpu_baseline(c, g, params, target_s: float):
             "seconds": t_ent + t_plain, "host": host_desc()}
 
 
+
+def reference_package_sample(c, g, params, seconds: float = 8.0):
+    """The reference package itself (baseline/_ref: the unmodified `nent`,
+    numpy + numba, single-threaded by design) on a bounded cfg2 sample through
+    its public API: entangle -> apply_entangled(CIRCULAR_CONVOLUTION on the
+    zero-padded streams) -> disentangle(failed=None), the stages its own
+    bench.py times (pkg/src/nent/bench.py:74-125).  None when not installed."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "nent").is_dir():
+        return None
+    code = r"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import nent
+c = np.load(sys.argv[2]); g = np.load(sys.argv[3])
+p = nent.CodecParams(*[int(v) for v in sys.argv[4].split(",")])
+budget = float(sys.argv[5])
+K = len(g)
+def run(ns):
+    pad = np.zeros((c.shape[0], ns + K - 1), dtype=np.int64); pad[:, :ns] = c[:, :ns]
+    op = nent.LsbOp(nent.OpKind.CIRCULAR_CONVOLUTION, nent.Kernel.of_vector(g))
+    t0 = time.perf_counter()
+    e = nent.entangle(nent.StreamBlock(p, pad))
+    d = nent.apply_entangled(op, e)
+    out = nent.disentangle(d, failed=None)
+    t = time.perf_counter() - t0
+    t1 = time.perf_counter(); plain = nent.apply_conventional(op, nent.StreamBlock(p, pad)); tp = time.perf_counter() - t1
+    assert np.array_equal(out.data, plain.data)
+    return t, tp, out.data.size
+ns = 1 << 12
+t, tp, s = run(ns)
+ns = int(min(c.shape[1], max(ns, ns * budget / max(t, 1e-6))))
+t, tp, s = run(ns)
+print(json.dumps({"value": s / t, "plain_value": s / tp, "seconds": t + tp, "samples_per_stream": ns}))
+"""
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        cp, gp = Path(td) / "c.npy", Path(td) / "g.npy"
+        np.save(cp, np.ascontiguousarray(c[:, : 1 << 20]))
+        np.save(gp, g)
+        try:
+            r = subprocess.run([sys.executable, "-c", code, str(ref), str(cp), str(gp),
+                                f"{params.m},{params.w},{params.l},{params.k}", str(seconds)],
+                               capture_output=True, text=True, timeout=600,
+                               env=dict(os.environ, OMP_NUM_THREADS="1", NUMBA_NUM_THREADS="1"))
+            out = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            return {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    return {"value": out["value"], "unit": UNIT, "cores": 1, "kind": "reference",
+            "plain_value": out["plain_value"], "overhead_pct": (out["plain_value"] / out["value"] - 1) * 100,
+            "sample": f"first {out['samples_per_stream']} samples of each cfg2 stream through the unmodified "
+                      "nent package (baseline/_ref, numpy + numba, 1 thread): entangle -> apply_entangled(conv "
+                      "of the zero-padded streams) -> disentangle(failed=None)",
+            "seconds": out["seconds"]}
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return  # only rank 0 runs the CPU reference arm
     from oracle import oracle as O
 
-    params, c, g = make_inputs(0, 1 << 24, 256)
+    params, c, g = make_inputs(0, 1 << 24, 256, args.w)
     threads = host_threads()
     ns = 1 << 16  # bounded sample per step, sized so the run stays within a few minutes
     t, _, _ = cpu_pipeline_time(O, c[:, :ns], g, params, threads)
@@ -836,18 +1020,19 @@ def run_reference(args):
         tp.append(b)
     t_step = sum(te) / len(te)
     value = samples / t_step
+    pkg = reference_package_sample(c, g, params)
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 (reference numpy semantics)",
         "data": "synthetic (canonical seeded cfg2 draw, SURVEY.md 8d)",
-        "config": {"workload": WORKLOAD, "sample": f"first {ns} samples per stream"},
+        "config": bench_config(world, args.w),
         "impl": "reference",
         "overhead_pct": statistics.median([(a - b) / b * 100 for a, b in zip(te, tp)]),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"first {ns} samples of each cfg2 stream per step (K=256, full "
                                    f"conv, entangle+conv+recover), oracle/nent_oracle.c OpenMP",
-                         "host": host_desc()},
+                         "host": host_desc(), "reference_package": pkg},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 

@@ -60,6 +60,11 @@ extern "C" {
  * (fused extract when `extract`) with K taps runs: 2 = tcgen05, 1 = mma.sync,
  * 0 = not an IMMA flavour. */
 int nent_imma_kernel(int flavor, int K, int rows, int extract);
+/* The convolution kernel the calling host thread launched last (diagnostic,
+ * for tests and the benchmark): 1 CUDA-core tile kernel, 2 mma.sync digit
+ * slicing, 3 tcgen05 digit slicing, 4 tcgen05 fused m = 3 with l = 16
+ * (conv_tc05_m3.cu), 0 none yet. */
+int nent_last_conv_kernel(void);
 
 /* Elementwise op codes (ops.py:193-204). */
 #define NENT_EW_ADD 0

@@ -132,10 +132,11 @@ def taps_tensor(g, flavor: int | None = None) -> torch.Tensor:
 
 # ------------------------------------------------------------------- codec --
 
-def entangle(c: torch.Tensor, l: int, check_hi: int | None = None, out_dtype=torch.int64):
+def entangle(c: torch.Tensor, l: int, check_hi: int | None = None, out_dtype=torch.int64,
+             out: torch.Tensor | None = None):
     """K1: returns (eps, first_bad_linear_index or None)."""
     m, n = c.shape
-    eps = torch.empty((m, n), dtype=out_dtype, device=c.device)
+    eps = torch.empty((m, n), dtype=out_dtype, device=c.device) if out is None else out
     bad = _status() if check_hi is not None else None
     call("nent_entangle", row_ptrs(c), bits(c), row_ptrs(eps), bits(eps), m, n, l,
          -1 if check_hi is None else int(check_hi), ptr(bad), _sh())
@@ -272,6 +273,12 @@ def imma_kernel(flavor: int, K: int, rows: int, extract: bool) -> str:
     """Which tensor-core kernel an IMMA flavour runs for this shape."""
     return {0: "cuda-core", 1: "mma.sync", 2: "tcgen05"}[
         _lib.lib().nent_imma_kernel(int(flavor), int(K), int(rows), int(bool(extract)))]
+
+
+def last_conv_kernel() -> str:
+    """The convolution kernel this host thread launched last."""
+    return {0: "none", 1: "cuda-core", 2: "mma.sync", 3: "tcgen05", 4: "tcgen05_m3"}[
+        _lib.lib().nent_last_conv_kernel()]
 
 
 def copy_rows(dst: torch.Tensor, src: torch.Tensor) -> None:

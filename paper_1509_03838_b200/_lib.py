@@ -88,6 +88,7 @@ SIGNATURES = {
     "nent_checksum_encode": [_PP, _I, _I, _L, _P, _I, _P],
     "nent_checksum_recover": [_PP, _I, _P, _I, _I, _L, _I, _P, _I, _P],
     "nent_imma_kernel": [_I, _I, _I, _I],
+    "nent_last_conv_kernel": [],
     "nent_extract_verify": [_PP, _I, _PP, _I, _I, _L, _I, _I, _I, _P, _P, _P],
     "nent_copy_rows": [_P, _L, _P, _L, _L, _I, _I, _P],
     "nent_microbench": [_I, _I, _I, _I, _P, ctypes.POINTER(ctypes.c_double), _P],

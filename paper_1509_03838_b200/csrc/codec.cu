@@ -5,6 +5,10 @@
 #include <cstdio>
 
 #include "common.cuh"
+
+#include <map>
+#include <mutex>
+#include <utility>
 #include "recover.cuh"
 
 namespace nent {
@@ -17,6 +21,44 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof g_err, fmt, ap);
   va_end(ap);
 }
+
+static thread_local int g_last_conv_kernel = 0;
+
+namespace {
+std::mutex g_dev_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_cfg;  // (device, kernel) -> opted-in bytes
+int g_sms[64];                                              // 0 unknown, -1 not sm_100
+}  // namespace
+
+int ensure_smem(const void* kern, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  size_t& have = g_smem_cfg[{dev, kern}];
+  if (bytes <= have) return NENT_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+    set_error("cannot reserve %zu bytes of shared memory on device %d", bytes, dev);
+    return NENT_ERR_CUDA;
+  }
+  have = bytes;
+  return NENT_OK;
+}
+
+int sm100_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  int& n = g_sms[dev & 63];
+  if (n == 0) {
+    int sms = 0, major = 0, minor = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    n = (major == 10 && minor == 0 && sms > 0) ? sms : -1;
+  }
+  return n;
+}
+void note_conv_kernel(int k) { g_last_conv_kernel = k; }
 
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -212,6 +254,7 @@ extern "C" {
 
 const char* nent_last_error(void) { return g_err; }
 int nent_abi_version(void) { return NENT_ABI_VERSION; }
+int nent_last_conv_kernel(void) { return nent::g_last_conv_kernel; }
 
 int nent_enable_peer_access(int peer) {
   int dev = 0;

@@ -35,6 +35,15 @@ inline MutRows to_mrows(void* const* p, int k) {
   return r;
 }
 int check_launch(const char* what);
+// the convolution kernel the calling host thread launched last
+// (nent_last_conv_kernel): 1 CUDA-core, 2 mma.sync, 3 tcgen05, 4 tcgen05 fused m = 3
+void note_conv_kernel(int k);
+// Dynamic shared memory opt-in of `kern` on the current device, done once
+// per (device, kernel) and size (thread-safe): NENT_OK or NENT_ERR_CUDA.
+int ensure_smem(const void* kern, size_t bytes);
+// SM count of the current device when it is an sm_100 part, else -1
+// (cached per device ordinal).
+int sm100_sms();
 
 __device__ __forceinline__ int64_t wshl(int64_t x, int s) { return (int64_t)((uint64_t)x << s); }
 __device__ __forceinline__ int64_t wadd(int64_t a, int64_t b) { return (int64_t)((uint64_t)a + (uint64_t)b); }

@@ -305,15 +305,7 @@ static int launch_conv(ConvArgs A, cudaStream_t stream) {
   A.gbytes = (int)((kseg * sizeof(typename MT::GT) + 15) & ~(size_t)15);
   const size_t smem = (size_t)A.gbytes + (size_t)MS * MT::NX * A.sstride * sizeof(typename MT::XT);
   auto kern = conv_tile_kernel<FLAV, MS, EXTRACT>;
-  static size_t configured = 0;
-  if (smem > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
-      set_error("conv: cannot reserve %zu bytes of shared memory", smem);
-      return NENT_ERR_CUDA;
-    }
-    configured = smem;
-  }
+  if (ensure_smem((const void*)kern, smem) != NENT_OK) return NENT_ERR_CUDA;
   const int64_t tiles = (A.n_out + T - 1) / T;
   if (tiles > 0x7fffffffLL) {
     set_error("conv: too many tiles");
@@ -321,6 +313,7 @@ static int launch_conv(ConvArgs A, cudaStream_t stream) {
   }
   dim3 grid((unsigned)tiles, EXTRACT ? 1 : (unsigned)((A.rows + MS - 1) / MS));
   kern<<<grid, CV_NT, smem, stream>>>(A);
+  note_conv_kernel(1);
   return check_launch("conv");
 }
 

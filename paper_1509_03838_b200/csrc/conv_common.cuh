@@ -100,5 +100,8 @@ __device__ __forceinline__ void stage_row(const ConvArgs& A, int row, int64_t p0
 int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s);
 constexpr int NENT_TC05_NA = 1000;  // tc05_conv: shape outside the tcgen05 kernel's envelope
 int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s);
+// fused m = 3 with the byte-aligned shift l = 16 (conv_tc05_m3.cu), or NENT_TC05_NA
+int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s);
+bool tc05_m3_envelope(const ConvArgs& A, int np, int ng);
 
 }  // namespace nent

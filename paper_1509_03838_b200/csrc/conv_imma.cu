@@ -416,15 +416,7 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
     return NENT_ERR_PARAM;
   }
   auto kern = conv_imma_kernel<MS, NG, EXTRACT>;
-  static size_t configured = 0;
-  if (Gm.smem > configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm.smem) !=
-        cudaSuccess) {
-      set_error("imma conv: cannot reserve %zu bytes of shared memory", Gm.smem);
-      return NENT_ERR_CUDA;
-    }
-    configured = Gm.smem;
-  }
+  if (ensure_smem((const void*)kern, Gm.smem) != NENT_OK) return NENT_ERR_CUDA;
   // digit-split Toeplitz taps: the caller's prepared table, or one built for
   // this launch in a stream-ordered workspace (freed in stream order after it)
   unsigned char* table = nullptr;
@@ -442,6 +434,7 @@ static int launch_imma(ConvArgs A, int np, cudaStream_t stream) {
   const int64_t tiles = (A.n_out + T - 1) / T;
   dim3 grid((unsigned)tiles, EXTRACT ? 1 : (unsigned)((A.rows + MS - 1) / MS));
   kern<<<grid, IM_NT, Gm.smem, stream>>>(A, Gm);
+  note_conv_kernel(2);
   const int st = check_launch("imma conv");
   if (table) cudaFreeAsync(table, stream);
   return st;
@@ -477,6 +470,10 @@ int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
     return NENT_ERR_PARAM;
   }
   if (!(flavor & NENT_IMMA_MMA_SYNC)) {
+    if (extract) {
+      const int st = tc05_fused_m3(A, np, ng, s);
+      if (st != NENT_TC05_NA) return st;
+    }
     const int st = tc05_conv(A, np, ng, extract, s);
     if (st != NENT_TC05_NA) return st;
   }

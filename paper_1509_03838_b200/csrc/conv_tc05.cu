@@ -23,18 +23,7 @@ static KernFn kernel_for(bool extract, int si, int np, int ng) {
 }
 }  // namespace tcc
 
-static int sm_count_tc() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    int major = 0;
-    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-    if (major != 10) n = -1;  // tcgen05 is sm_100-family only
-  }
-  return n;
-}
+static int sm_count_tc() { return sm100_sms(); }  // tcgen05 is sm_100-family only
 
 // Returns NENT_TC05_NA when the shape is outside this kernel's envelope (the
 // caller then runs the mma.sync kernel), else a NENT status.
@@ -76,7 +65,17 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
   // fused with a failed stream: only the two survivors are convolved (the
   // failed stream's delta is never produced, as in the reference's recovery)
   if (extract && A.r >= 0) G.nstreams = 2;
-  { const char* e = getenv("NENT_TC05_DEBUG"); G.debug = e ? atoi(e) : 0; }
+#if defined(NENT_TC05_PROFILING) || defined(NENT_TC05_TIMERS)
+  // profiling builds only (scripts/build_variant.py): role-isolation modes
+  // that skip work, read once per process
+  static const int debug_env = [] {
+    const char* e = getenv("NENT_TC05_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  G.debug = debug_env;
+#else
+  G.debug = 0;  // release: every role always runs
+#endif
   const int sms = sm_count_tc();
   if (sms <= 0) return NENT_TC05_NA;
   {  // align the input windows: (row-0 word offset + P0) = 0 mod 4
@@ -88,14 +87,7 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
   const int si = G.nsteps / 4 - 1;
   const KernFn kern = kernel_for(extract, si, np, ng);
   if (!kern) return NENT_TC05_NA;
-  static size_t configured[2][3][6][4] = {};
-  if (smem > configured[extract][si][np - 1][ng - 1]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-      set_error("tc05 conv: cannot reserve %zu bytes of shared memory", smem);
-      return NENT_ERR_CUDA;
-    }
-    configured[extract][si][np - 1][ng - 1] = smem;
-  }
+  if (ensure_smem((const void*)kern, smem) != NENT_OK) return NENT_ERR_CUDA;
   static unsigned long long* dbg = nullptr;
   if (G.debug & 8) {
     if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
@@ -132,6 +124,7 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s) {
             h[1] / 1e3 / grid, h[2] / 1e3 / grid, h[3] / 1e3 / grid, h[4] / 1e3 / grid, h[5] / 1e3 / grid,
             h[6] / 1e3 / grid, h[7] / 1e3 / grid, h[8] / 1e3 / grid, h[9] / 1e3 / grid, h[10] / 1e3);
   }
+  note_conv_kernel(3);
   return check_launch("tc05 conv");
 }
 

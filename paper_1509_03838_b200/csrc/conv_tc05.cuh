@@ -577,6 +577,11 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_kernel(const __grid_constant_
           if (!(G.debug & 4096)) tc05::commit_elect(empty_b(slot));
         }
       }
+      // drain the last plane slots' commits before the CTA can exit: an
+      // mbarrier arrive still in flight must not land in a successor CTA's
+      // shared memory
+      if (!(G.debug & 4096))
+        for (int s = seq > 2 ? seq - 2 : 0; s < seq; ++s) mb_wait(empty_b(s & 1), (uint32_t)((s >> 1) & 1));
     }
     __syncwarp();
   } else if (!epi_warp) {

@@ -1,0 +1,68 @@
+// conv_tc05_m3.cu -- host side of the m = 3, byte-aligned-shift fused kernel
+// (conv_tc05_m3.cuh): envelope, geometry and launch.  Shapes outside the
+// envelope return NENT_TC05_NA and take the generic tcgen05 kernel.
+#include "conv_tc05_m3.cuh"
+
+#include <cstdlib>
+
+namespace nent {
+namespace tcm3 {
+using KernFn = void (*)(ConvArgs, Geom);
+
+static KernFn kernel_for(int nsteps, int ng) {
+  static const KernFn tab[3][2] = {{conv_tc05_m3_kernel<1, 4>, conv_tc05_m3_kernel<2, 4>},
+                                   {conv_tc05_m3_kernel<1, 8>, conv_tc05_m3_kernel<2, 8>},
+                                   {conv_tc05_m3_kernel<1, 12>, conv_tc05_m3_kernel<2, 12>}};
+  if (ng < 1 || ng > 2 || nsteps % 4 || nsteps < 4 || nsteps > 12) return nullptr;
+  return tab[nsteps / 4 - 1][ng - 1];
+}
+
+}  // namespace tcm3
+
+bool tc05_m3_envelope(const ConvArgs& A, int np, int ng) {
+  using namespace tcm3;
+  if (A.rows != 3 || A.in_bits != 32 || A.y_bits != 32 || A.l != 16 || np != 4 || ng < 1 || ng > 2) return false;
+  for (int i = 0; i < 3; ++i)
+    if (!A.a.p[i] || !A.b.p[i] || !A.y.p[i]) return false;  // raw streams, entangled on load
+  if (A.perm || A.add || A.scale != 1 || A.wide) return false;
+  if (A.period < A.n_in + A.K - 1) return false;  // zero-padded (full) convolution only
+  if (A.K < 1 || A.K > 257) return false;
+  for (int i = 0; i < 3; ++i)  // int32 rows: 4-byte aligned
+    if (reinterpret_cast<uintptr_t>(A.b.p[i]) & 3) return false;
+  // every class accumulator is an exact int32: |sum| <= 2^15 K min(4, ng)
+  if ((int64_t)32768 * A.K * ng >= ((int64_t)1 << 31)) return false;
+  return true;
+}
+
+int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
+  using namespace tcm3;
+  // A/B switch for measurements (read once): NENT_TC05_M3=0 routes these
+  // shapes to the generic tcgen05 kernel, which is exact too
+  static const bool enabled = [] {
+    const char* e = getenv("NENT_TC05_M3");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!enabled || !tc05_m3_envelope(A, np, ng)) return NENT_TC05_NA;
+  const int sms = sm100_sms();
+  if (sms <= 0) return NENT_TC05_NA;
+  Geom G{};
+  G.KT = (A.K + 127 + 127) / 128 * 128;
+  G.nsteps = G.KT / 32;
+  if (8 * ng * G.nsteps > TAPCOLS) return NENT_TC05_NA;
+  {  // tiles start `shift` outputs early so every input window is 16-byte aligned
+    const int64_t wb = (int64_t)((reinterpret_cast<uintptr_t>(A.b.p[0]) >> 2) & 3);
+    G.shift = (int)(((wb + A.y_begin - G.KT + 128) % 4 + 4) % 4);
+  }
+  for (int i = 0; i < 3; ++i)
+    G.dph[i] = (int)((((reinterpret_cast<uintptr_t>(A.b.p[i]) - reinterpret_cast<uintptr_t>(A.b.p[0])) >> 2) % 4 + 4) % 4);
+  G.ntiles = (A.n_out + G.shift + TILE - 1) / TILE;
+  const KernFn kern = kernel_for(G.nsteps, ng);
+  if (!kern) return NENT_TC05_NA;
+  if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
+  const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
+  kern<<<grid, NT, SMEM, s>>>(A, G);
+  note_conv_kernel(4);
+  return check_launch("tc05 fused m3");
+}
+
+}  // namespace nent

@@ -1,0 +1,469 @@
+// conv_tc05_m3.cuh -- the cfg2 hot path: fused entangle -> convolution ->
+// extract of m = 3 int32 streams on the 5th-generation tensor cores, for a
+// byte-aligned entangling shift (l = 16, the (3,48,16,16) geometry) and
+// samples with |c| <= 0x7F7F.  Reference semantics: codec.entangle
+// (codec.py:57-72), ops._circ_conv_rows on the zero-padded streams
+// (ops.py:158-172), codec.disentangle (codec.py:89-131).
+//
+// Entangling on load, by digit placement.  With l = 16 the entangled word
+// eps_i = (c_{i-1} << 16) + c_i of samples |c| <= 0x7F7F has, as its four
+// unsigned base-256 digits (u = eps + 0x80808080, the operand the MMA reads),
+// exactly the two bytes of c_i + 0x8080 followed by the two bytes of
+// c_{i-1} + 0x8080: no carry crosses the 16-bit boundary.  So the producers
+// split each raw stream of a tile ONCE into two byte planes, and the MMA
+// convolves eps_i by reading planes {lo(c_i), hi(c_i), lo(c_{i-1}),
+// hi(c_{i-1})} -- the four digit planes of the entangled word.  The tensor
+// core does the full entangled arithmetic (4 data digits x NG tap digits per
+// stream, the same MACs as the generic kernel); only the digit extraction is
+// shared between the two streams a sample is entangled into.
+//
+// Extraction in registers with no shared-memory stash: the MMA issues the
+// classes of the two recovery streams interleaved (class c of stream P+1,
+// then class c of stream P+2), so every epilogue thread holds both deltas of
+// its 16 outputs at once and recovers d_P, d_{P+1}, d_{P+2}; with failed =
+// None the redundant stream P follows and is checked against the recovery.
+//
+// CTA: 20 warps = 5 warpgroups, one persistent CTA per SM; a tile is 48
+// blocks of 128 outputs (MMA N = 48) of each stream.
+//   warps 0-11  epilogue (3 per TMEM lane quadrant, 16 accumulator columns
+//               each; 128 registers after setmaxnreg)
+//   warps 12-18 producers: TMA bulk copies of the raw int32 windows into a
+//               3-deep staging ring, split into byte planes (2 tile slots)
+//   warp 19     TMEM allocation; one elected lane issues every tcgen05.mma
+// TMEM: [0, 8*NG*NSTEPS) the Toeplitz tap digits (A operand), [192, 480) a
+// ring of 6 accumulator slots of 48 columns.
+#pragma once
+#include "conv_tc05.cuh"
+
+#include <cstdio>
+
+namespace nent {
+namespace tcm3 {
+
+using tcc::bias_of;
+using tcc::bulk_g2s;
+using tcc::digits_of;
+using tcc::elect_one;
+using tcc::fence_async_smem;
+using tcc::mb_arrive;
+using tcc::mb_expect_tx;
+using tcc::mb_init;
+using tcc::mb_wait;
+using tcc::mb_wait_sleep;
+using tcc::sts32;
+
+constexpr int U = 48;                  // 128-position blocks per tile = MMA N
+constexpr int TILE = 128 * U;          // outputs per tile and stream
+constexpr int NEPI = 12;               // epilogue warps (3 per TMEM lane quadrant)
+constexpr int NPROD = 7;               // producer warps
+constexpr int MMA_WARP = NEPI + NPROD; // 19
+constexpr int NT = 32 * (NEPI + NPROD + 1);
+constexpr int EC = U / (NEPI / 4);     // 16 accumulator columns per epilogue thread
+constexpr int PT = 32 * NPROD;         // producer threads
+constexpr int HALFW = 4;               // int4 words per producer thread and half window
+constexpr int NWP = 2 * HALFW * PT;    // int4 words staged per raw stream and tile (1792)
+constexpr uint32_t HALFB = HALFW * PT * 16;  // bytes per staging unit (14,336)
+constexpr int NSTAGE = 3;              // staging ring depth (TMA runs two units ahead)
+constexpr int PLANE = 7168;            // bytes per byte plane: >= 4 * NWP, 1024-aligned
+constexpr int SLOTB = 6 * PLANE;       // one tile slot: 3 raw streams x {lo, hi}
+constexpr int TAPCOLS = 192;
+constexpr int RING0 = TAPCOLS;
+constexpr int SLOTS = (512 - RING0) / U;  // 6
+constexpr int LAUNCH_REGS = 96;        // 65536 / 640 rounded down to 8
+constexpr int EPI_REGS = 128, PROD_REGS = 48;
+static_assert(NEPI * 32 * EPI_REGS + (NPROD + 1) * 32 * PROD_REGS <= NT * LAUNCH_REGS, "launch register pool");
+static_assert(NEPI % 4 == 0 && (NPROD + 1) % 4 == 0, "setmaxnreg acts on whole warpgroups");
+static_assert(4 * NWP >= TILE + 256, "a staged window covers the tile plus the K <= 257 halo");
+static_assert(4 * NWP <= PLANE, "a staged window fits its plane");
+constexpr uint32_t SSTR = HALFB + 128;  // staging slot stride: a unit plus one int4 of lead-in
+constexpr size_t SMEM = 2 * (size_t)SLOTB + NSTAGE * (size_t)SSTR;  // 129,408 B
+
+struct Geom {
+  int KT, nsteps;
+  int64_t ntiles;
+  int shift;   // tiles start `shift` outputs early: row 0's windows are 16-byte aligned
+  int dph[3];  // word phase of row s relative to row 0 (mod 4): its windows are
+               // copied from dph[s] words earlier and read shifted in shared memory
+};
+
+// u = c + 0x8080 of 4 consecutive samples -> the lo-byte and hi-byte plane words
+__device__ __forceinline__ void split2(int4 v, uint32_t& lo, uint32_t& hi) {
+  const uint32_t u0 = (uint32_t)v.x + 0x8080u, u1 = (uint32_t)v.y + 0x8080u;
+  const uint32_t u2 = (uint32_t)v.z + 0x8080u, u3 = (uint32_t)v.w + 0x8080u;
+  const uint32_t t01 = __byte_perm(u0, u1, 0x5140), t23 = __byte_perm(u2, u3, 0x5140);
+  lo = __byte_perm(t01, t23, 0x5410);
+  hi = __byte_perm(t01, t23, 0x7632);
+}
+
+// Register pins: an empty volatile asm that reads and rewrites x, ordered
+// with the other volatile asm (the next TMEM drain): the class fold before it
+// completes first, instead of being sunk below the next drain (which would
+// keep two classes' registers live and spill).
+__device__ __forceinline__ void pin(uint64_t& x) { asm volatile("" : "+l"(x)); }
+__device__ __forceinline__ void pin(uint32_t& x) { asm volatile("" : "+r"(x)); }
+
+// the chains (data digit p, tap digit j) of digit class c, in a fixed order
+template <int NG, typename F>
+__device__ __forceinline__ void for_class(int c, F&& f) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int j = c - p;
+    if (j >= 0 && j < NG) f(p, j);
+  }
+}
+
+template <int NG, int NSTEPS>
+__global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_constant__ ConvArgs A,
+                                                             const __grid_constant__ Geom G) {
+  constexpr int NCLS = 4 + NG - 1;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // full[2], empty[2], stage full[3], stage empty[3], acc full[5], acc empty[5]
+  __shared__ __align__(8) uint64_t bars[4 + 2 * NSTAGE + 2 * SLOTS];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t planes_s = tc05::smem_u32(smem_raw);
+  const uint32_t stage_s = planes_s + 2u * SLOTB;
+  const uint32_t bar0 = tc05::smem_u32(bars);
+  auto full_b = [&](int s) { return bar0 + 8u * (uint32_t)s; };
+  auto empty_b = [&](int s) { return bar0 + 8u * (uint32_t)(2 + s); };
+  auto stg_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + s); };
+  auto stge_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + NSTAGE + s); };
+  auto accf_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + 2 * NSTAGE + s); };
+  auto acce_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + 2 * NSTAGE + SLOTS + s); };
+
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mb_init(full_b(s), PT);
+      mb_init(empty_b(s), 1);
+    }
+    for (int s = 0; s < NSTAGE; ++s) {
+      mb_init(stg_b(s), 1);
+      mb_init(stge_b(s), PT);
+    }
+    for (int s = 0; s < SLOTS; ++s) {
+      mb_init(accf_b(s), 1);
+      mb_init(acce_b(s), NEPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) tc05::alloc(&tmem_slot, 512);
+  tc05::fence_before();
+  __syncthreads();
+  tc05::fence_after();
+  if (tmem_slot != 0 || (planes_s & 1023u)) __trap();
+  constexpr uint32_t tbase = 0;
+  {
+    // the reversed taps' digits, staged once in the (still free) staging ring:
+    // rev[j][i] = digit_j(g[KT-1-i]), A_j[v][k] = rev[j][k - v + 127]
+    const int RL = G.KT + 128;
+    unsigned char* rev = smem_raw + 2 * SLOTB;
+    const uint64_t gbias = bias_of(NG);
+    for (int i = tid; i < RL; i += NT) {
+      const int idx = G.KT - 1 - i;
+      const int64_t gv = (idx >= 0 && idx < A.K) ? ld_bits(A.g, A.g_bits, idx) : 0;
+      const uint64_t d = digits_of(gv, gbias);
+      for (int j = 0; j < NG; ++j) rev[j * RL + i] = (unsigned char)(d >> (8 * j));
+    }
+    __syncthreads();
+    const int v = 32 * (warp & 3) + lane;
+    for (int blk = warp >> 2; blk < NG * NSTEPS; blk += NT / 128) {
+      const int j = blk / NSTEPS, kc = blk % NSTEPS;
+      const unsigned char* r = rev + j * RL + 32 * kc - v + 127;
+      uint32_t w[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        w[c] = (uint32_t)r[4 * c] | ((uint32_t)r[4 * c + 1] << 8) | ((uint32_t)r[4 * c + 2] << 16) |
+               ((uint32_t)r[4 * c + 3] << 24);
+      tc05::st_x8(tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 8u * (uint32_t)blk, w);
+    }
+    tc05::wait_st();
+    tc05::fence_before();
+    __syncthreads();
+    tc05::fence_after();
+  }
+  const bool verify = A.r < 0;
+  const int P = verify ? 0 : A.r;  // pivot: the stream never read (or checked last)
+  const int sA = P + 1 >= 3 ? P - 2 : P + 1, sB = P + 2 >= 3 ? P - 1 : P + 2;
+  const int64_t my_tiles = G.ntiles > blockIdx.x ? (G.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp < NEPI) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
+    // ---------------- epilogue ----------------
+    const int quad = warp & 3, part = warp >> 2;
+    const uint32_t lrow = (uint32_t)(32 * quad) << 16;
+    const int v = 32 * quad + lane;
+    uint64_t gsum = 0;
+    for (int k = lane; k < A.K; k += 32) gsum += (uint64_t)ld_bits(A.g, A.g_bits, k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+    // unsigned data digits carry +128 each: every delta is high by 128 * sum(g) * 0x01010101
+    const uint64_t corr = 0 - 128 * gsum * 0x01010101ull;
+    unsigned bad = 0;
+    int kslot = 0;  // running accumulator-slot use (same sequence as the MMA warp)
+    // TMEM -> registers for the next ring slot, which is then handed back to
+    // the MMA warp
+    auto drain = [&](uint32_t (&r)[EC]) {
+      const int rs = kslot % SLOTS;
+      mb_wait_sleep(accf_b(rs), (uint32_t)((kslot / SLOTS) & 1));
+      tc05::fence_after();
+#ifndef NENT_M3_DBG_NOLD
+      tc05::ld_x16(tbase + lrow + (uint32_t)(RING0 + rs * U + EC * part), r);
+#else
+      for (int i = 0; i < EC; ++i) r[i] = 0;
+#endif
+      tc05::wait_ld();
+      tc05::fence_before();
+      __syncwarp();
+      if (lane == 0) mb_arrive(acce_b(rs));
+      ++kslot;
+    };
+    int32_t* yP = reinterpret_cast<int32_t*>(A.y.p[P]);
+    int32_t* yA = reinterpret_cast<int32_t*>(A.y.p[sA]);
+    int32_t* yB = reinterpret_cast<int32_t*>(A.y.p[sB]);
+    for (int64_t t = 0; t < my_tiles; ++t) {
+      const int64_t tile = blockIdx.x + t * gridDim.x;
+      const int64_t ybase = tile * TILE - G.shift;
+      const int64_t o0 = ybase + 128 * (EC * part) + v;
+      const bool interior = ybase >= 0 && ybase + TILE <= A.n_out;
+      // Recovery from delta_A = delta_{P+1} = (d_P << 16) + d_{P+1} and
+      // delta_B = delta_{P+2} = (d_{P+1} << 16) + d_{P+2}, exact for the
+      // consistent words this kernel produces with int32 outputs (the
+      // y_bits == 32 contract; recover_rot_valid<3>, recover.cuh):
+      //   C = (delta_A << 16) - delta_B = (d_P << 32) - d_{P+2}   (mod 2^64)
+      //   d_{P+2} = -sext32(C),  d_P = hi32(C) - (C_lo < 0),
+      //   d_{P+1} = delta_A - (d_P << 16)                          (mod 2^32)
+      // so each output keeps one 64-bit and one 32-bit accumulator, folded
+      // class by class straight out of TMEM (class c carries weight 256^c).
+      uint64_t C[EC];
+      uint32_t lowA[EC];
+#pragma unroll
+      for (int i = 0; i < EC; ++i) {
+        C[i] = (corr << 16) - corr;
+        lowA[i] = (uint32_t)corr;
+      }
+      // a rolled class loop: the next class's TMEM load is not hoisted above
+      // this class's fold (which would keep extra registers live and spill)
+#pragma unroll 1
+      for (int c = 0; c < NCLS; ++c) {
+        uint32_t r[EC];
+        const int sh = 8 * c;
+        drain(r);  // class c of delta_A
+#pragma unroll
+        for (int i = 0; i < EC; ++i) {
+          const int64_t ra = (int64_t)(int32_t)r[i];
+          C[i] += (uint64_t)ra << (sh + 16);
+          lowA[i] += r[i] << sh;  // c = 4 adds r << 32 = 0 (mod 2^32)
+        }
+        drain(r);  // class c of delta_B
+#pragma unroll
+        for (int i = 0; i < EC; ++i) C[i] -= (uint64_t)(int64_t)(int32_t)r[i] << sh;
+      }
+      uint64_t accP[EC];
+#pragma unroll
+      for (int i = 0; i < EC; ++i) {
+        const int32_t vv = (int32_t)(uint32_t)C[i];  // = -d_{P+2}
+        const int32_t d0 = (int32_t)(uint32_t)(C[i] >> 32) - (vv >> 31);
+        const int32_t d1 = (int32_t)(lowA[i] - ((uint32_t)d0 << 16));
+        const int64_t o = o0 + 128 * i;
+#ifdef NENT_M3_DBG_NOSTORE
+        if (false) {
+#else
+        if (interior || (o >= 0 && o < A.n_out)) {
+#endif
+#ifdef NENT_M3_CHECK
+          if (o < 0 || o >= A.n_out) {
+            printf("M3CHECK store cta %d tile %lld o %lld n_out %lld\n", blockIdx.x, (long long)tile, (long long)o,
+                   (long long)A.n_out);
+            __trap();
+          }
+#endif
+          yP[o] = d0;
+          yA[o] = d1;
+          yB[o] = (int32_t)(0u - (uint32_t)vv);
+        }
+        // with failed = None the redundant word delta_P must equal
+        // (d_{P+2} << 16) + d_P: start its fold at minus that
+        accP[i] = corr - ((uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << 16));
+      }
+      if (verify) {
+#pragma unroll 1
+        for (int c = 0; c < NCLS; ++c) {
+          uint32_t r[EC];
+          drain(r);
+#pragma unroll
+          for (int i = 0; i < EC; ++i) accP[i] += (uint64_t)(int64_t)(int32_t)r[i] << (8 * c);
+        }
+#pragma unroll
+        for (int i = 0; i < EC; ++i) {
+          const int64_t o = o0 + 128 * i;
+          bad += (interior || (o >= 0 && o < A.n_out)) && accP[i] != 0;
+        }
+      }
+    }
+    if (A.mismatch) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      if (lane == 0 && bad) atomicAdd(A.mismatch, (unsigned long long)bad);
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PROD_REGS));
+    if (warp == MMA_WARP) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = tc05::idesc_i8(128, U, /*b_signed=*/false);
+      int kslot = 0;
+      for (int64_t t = 0; t < my_tiles; ++t) {
+        const int ts = (int)(t & 1);
+        mb_wait(full_b(ts), (uint32_t)((t >> 1) & 1));
+        tc05::fence_after();
+        if (elect_one()) {
+          const uint32_t slot_s = planes_s + (uint32_t)(ts * SLOTB);
+          // chains of stream i's class c into the next ring slot
+          auto issue_class = [&](int i, int c) {
+            const int rs = kslot % SLOTS, use = kslot / SLOTS;
+            if (use >= 1) {
+              mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1));
+              tc05::fence_after();
+            }
+            const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
+            const int im1 = i == 0 ? 2 : i - 1;
+            bool first = true;
+            for_class<NG>(c, [&](int p, int j) {
+              // data digit p of eps_i: bytes of c_i (p < 2) or of c_{i-1} (p >= 2)
+              const int raw = p < 2 ? i : im1;
+              const uint32_t blo0 = tc05::desc_sw128_lo(slot_s + (uint32_t)((2 * raw + (p & 1)) * PLANE));
+              const uint32_t a = tbase + (uint32_t)(8 * j * NSTEPS);
+#ifndef NENT_M3_DBG_NOMMA
+#pragma unroll
+              for (int kc = 0; kc < NSTEPS; ++kc)
+                tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
+#endif
+              first = false;
+            });
+            tc05::commit(accf_b(rs));
+            ++kslot;
+          };
+#pragma unroll
+          for (int c = 0; c < NCLS; ++c) {
+            issue_class(sA, c);
+            issue_class(sB, c);
+          }
+          if (verify) {
+#pragma unroll
+            for (int c = 0; c < NCLS; ++c) issue_class(P, c);
+          }
+          tc05::commit(empty_b(ts));
+        }
+        __syncwarp();
+      }
+      // drain the last tiles' commits before the CTA can exit: an mbarrier
+      // arrive still in flight must not land in a successor CTA's shared memory
+      for (int64_t t = my_tiles > 2 ? my_tiles - 2 : 0; t < my_tiles; ++t)
+        mb_wait(empty_b((int)(t & 1)), (uint32_t)((t >> 1) & 1));
+    } else {
+      // ---------------- producers ----------------
+      const int ptid = tid - 32 * NEPI;  // 0 .. PT-1
+      const int64_t units = my_tiles * 6;
+      // unit H: tile t = H / 6, raw stream s = (H % 6) / 2, half h = H % 2.
+      // mode 1: the window is inside [0, n_in) -> TMA bulk copy into the ring;
+      // mode 2: per-thread loads with zero padding outside [0, n_in)
+      auto unit_P0 = [&](int64_t H) {
+        const int64_t tile = blockIdx.x + (H / 6) * gridDim.x;
+        return A.y_begin - G.shift + tile * TILE - (G.KT - 128);
+      };
+      auto unit_mode = [&](int64_t H) {
+        const int64_t P0 = unit_P0(H);
+#ifdef NENT_M3_DBG_NOTMA
+        return 2;
+#endif
+        return (P0 >= 4 && P0 + 4 * (int64_t)NWP + 4 <= A.n_in) ? 1 : 2;
+      };
+      // TMA issue (thread 0): units up to H + NSTAGE - 1, mode-1 units only,
+      // each into ring buffer (j % NSTAGE) for the j-th mode-1 unit
+      int64_t next_issue = 0, issued = 0, consumed = 0;
+      auto issue_upto = [&](int64_t Hmax) {
+        for (; next_issue < units && next_issue <= Hmax; ++next_issue) {
+          if (unit_mode(next_issue) != 1) continue;
+          const int b = (int)(issued % NSTAGE);
+          if (issued >= NSTAGE) mb_wait(stge_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1));
+          const int s = (int)((next_issue % 6) / 2), h = (int)(next_issue & 1);
+          const int d = G.dph[s];
+          const char* src = reinterpret_cast<const char*>(reinterpret_cast<const int32_t*>(A.b.p[s]) +
+                                                          unit_P0(next_issue) - d) + (size_t)h * HALFB;
+          const uint32_t bytes = HALFB + (d ? 16u : 0u);
+#ifdef NENT_M3_CHECK
+          if ((reinterpret_cast<uintptr_t>(src) & 15) || ((stage_s + (uint32_t)b * SSTR) & 15) || (bytes & 15) ||
+              unit_P0(next_issue) - d < 0 || unit_P0(next_issue) - d + (int64_t)h * HALFB / 4 + bytes / 4 > A.n_in) {
+            printf("M3CHECK tma cta %d unit %lld s %d h %d P0 %lld d %d src %p bytes %u n_in %lld\n", blockIdx.x,
+                   (long long)next_issue, s, h, (long long)unit_P0(next_issue), d, src, bytes, (long long)A.n_in);
+            __trap();
+          }
+#endif
+          mb_expect_tx(stg_b(b), bytes);
+          bulk_g2s(stage_s + (uint32_t)b * SSTR, src, bytes, stg_b(b));
+          ++issued;
+        }
+      };
+      for (int64_t H = 0; H < units; ++H) {
+        const int64_t t = H / 6;
+        const int ts = (int)(t & 1);
+        const int s = (int)((H % 6) / 2), h = (int)(H & 1);
+        if (H % 6 == 0 && t >= 2) mb_wait_sleep(empty_b(ts), (uint32_t)(((t >> 1) - 1) & 1));
+        if (ptid == 0) issue_upto(H + NSTAGE - 1);
+        const uint32_t plo = planes_s + (uint32_t)(ts * SLOTB + (2 * s) * PLANE);
+        int4 v[HALFW];
+        if (unit_mode(H) == 1) {
+          const int b = (int)(consumed % NSTAGE);
+          mb_wait_sleep(stg_b(b), (uint32_t)((consumed / NSTAGE) & 1));
+          const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
+          const int d = G.dph[s];
+          if (d == 0) {
+            const int4* sb = reinterpret_cast<const int4*>(__cvta_shared_to_generic(sbuf));
+#pragma unroll
+            for (int i = 0; i < HALFW; ++i) v[i] = sb[i * PT + ptid];
+          } else {  // this row's window starts d words into the staged copy
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d;
+#pragma unroll
+            for (int i = 0; i < HALFW; ++i) {
+              const uint32_t* q = sw + 4 * (i * PT + ptid);
+              v[i] = make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]);
+            }
+          }
+          mb_arrive(stge_b(b));  // this thread is done with the buffer
+          ++consumed;
+        } else {
+          const int32_t* bp = reinterpret_cast<const int32_t*>(A.b.p[s]);
+          const int64_t P0 = unit_P0(H);
+#pragma unroll
+          for (int i = 0; i < HALFW; ++i) {
+            const int64_t q0 = P0 + 4 * (int64_t)(ptid + PT * (HALFW * h + i));
+            int e[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) e[k] = (q0 + k >= 0 && q0 + k < A.n_in) ? __ldg(bp + q0 + k) : 0;
+            v[i] = make_int4(e[0], e[1], e[2], e[3]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < HALFW; ++i) {
+          uint32_t lo, hi;
+          split2(v[i], lo, hi);
+          const uint32_t off = tc05::sw128(4u * (uint32_t)(ptid + PT * (HALFW * h + i)));
+          sts32(plo + off, lo);
+          sts32(plo + (uint32_t)PLANE + off, hi);
+        }
+        if (H % 6 == 5) {
+          fence_async_smem();
+          mb_arrive(full_b(ts));
+        }
+      }
+    }
+  }
+  tc05::fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc05::fence_after();
+    tc05::dealloc(tbase, 512);
+  }
+}
+
+}  // namespace tcm3
+}  // namespace nent

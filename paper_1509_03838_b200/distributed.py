@@ -353,17 +353,20 @@ class HaloSplit:
             halo = xh.to(c_slice.device)
         return torch.cat([halo, c_slice], dim=1).contiguous()
 
+    def window(self, n: int) -> dict:
+        """The fused kernel's window over [halo | slice] for an n-sample slice:
+        the full convolution of the zero-extended row (period), the halo_width
+        lead-in skipped (y_begin), n outputs (+ the K-1 tail on the last rank)."""
+        H, Hp = self.K - 1, self.halo_width
+        last = self.rank == self.world - 1
+        return {"period": Hp + n + H, "n_in": Hp + n, "y_begin": Hp, "n_out": n + (H if last else 0)}
+
     def run(self, c_slice: torch.Tensor, g, failed: int | None = None):
         """Recovered full-convolution outputs owned by this rank: positions
         [start, start + n_slice) of the global output (+ the K-1 tail on the
         last rank)."""
-        H, Hp = self.K - 1, self.halo_width
         x = self.exchange_halo(c_slice)
-        n = c_slice.shape[1]
-        last = self.rank == self.world - 1
-        n_out = n + (H if last else 0)
-        return self.compute.fused_conv(x, self.params, g, period=Hp + n + H, n_in=Hp + n,
-                                       y_begin=Hp, n_out=n_out, failed=failed)
+        return self.compute.fused_conv(x, self.params, g, failed=failed, **self.window(c_slice.shape[1]))
 
     def gather(self, d_local: torch.Tensor, dst: int = 0):
         xdev = torch.device("cpu") if _host_exchange(self.group) else d_local.device

@@ -430,3 +430,88 @@ def test_interleave_chain_gather_records(oracle, m, n, dt):
     for pdt in (torch.int32, torch.int64):
         x = D.gather_records(rec, torch.from_numpy(perm).cuda().to(pdt))
         assert np.array_equal(x.cpu().numpy(), ref), pdt
+
+
+@pytest.mark.parametrize("K", [1, 64, 128, 129, 200, 256, 257])
+@pytest.mark.parametrize("n", [1, 97, 6144 - 255, 3 * 6144 + 77])
+def test_tcgen05_m3_fused_every_failure(oracle, n, K):
+    """The cfg2 hot-path kernel (conv_tc05_m3.cu: m = 3, l = 16, the digit
+    planes of eps_i taken from the byte planes of c_i and c_{i-1}, recovery
+    in registers) against the oracle: every failure index, edge-only and
+    multi-tile lengths, K at every tap-table size; it must be the kernel that
+    ran (tap digits ng = 1 and 2)."""
+    p = nent.derive_params(3, 48)  # (3, 48, 16, 16)
+    for bits_g, seed in ((7, 1), (12, 2)):
+        g = rand(K * 7 + seed, (K,), -(1 << bits_g), (1 << bits_g) - 1)
+        # samples as wide as the admitted output range allows (<= 0x7F7F)
+        lim = min(0x7F7F, (nent.output_range(p).hi - 1) // max(int(np.abs(g).sum()), 1))
+        c = rand(n + K + seed, (3, n), -lim, lim)
+        ref = oracle.full_conv(c, g)
+        x = torch.from_numpy(c).cuda().to(torch.int32)
+        fl = imma_flavor(D.signed_digits(lim * ((1 << p.l) + 1)), D.signed_digits(int(np.abs(g).max())))
+        assert (fl >> 8) & 15 == 4
+        for r in (None, 0, 1, 2):
+            res = fused.entangled_conv(nent.StreamBlock(p, x), g, failed=r, flavor=fl, out_dtype=torch.int32)
+            assert D.last_conv_kernel() == "tcgen05_m3"
+            assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), ref), (n, K, bits_g, r)
+            if r is None:
+                assert res.mismatches == 0
+
+
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_tcgen05_m3_windows_and_row_phases(oracle, off):
+    """Output windows [y_begin, y_begin + n_out) (halo-split shards) and row
+    bases at every 4-byte phase through the m = 3 kernel, including rows
+    whose 16-byte phases differ from each other (staged from the aligned
+    word below and read shifted)."""
+    n, K = 20000, 256
+    p = nent.derive_params(3, 48)
+    c = rand(off + 70, (3, n), -2048, 2047)
+    g = rand(off + 71, (K,), -2048, 2047)
+    ref = oracle.full_conv(c, g)
+    big = torch.zeros((3, n + 8), dtype=torch.int32, device="cuda")
+    big[:, off:off + n] = torch.from_numpy(c).to(torch.int32)
+    x = big[:, off:off + n]
+    L = n + K - 1
+    fl = imma_flavor(D.signed_digits(2048 * ((1 << p.l) + 1)), D.signed_digits(2048))
+    gd = D.taps_tensor(g, fl)
+    for y0, cnt in [(0, L), (1, 9000), (2, 6145), (3, 1), (255, 12000), (4321, L - 4321), (L - 5, 5)]:
+        for r in (None, 1):
+            mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+            out = torch.empty((3, cnt), dtype=torch.int32, device="cuda")
+            D.fused_conv(x, gd, K, p.l, fl, r, True, L, n_in=n, y_begin=y0, n_out=cnt, out=out,
+                         mismatch=mm if r is None else None)
+            assert D.last_conv_kernel() == "tcgen05_m3"
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref[:, y0:y0 + cnt]), (off, y0, cnt, r)
+            assert int(mm.item()) == 0
+    # rows at different 16-byte phases
+    rows = [big[0, off:off + n], big[1, (off + 1) % 4:(off + 1) % 4 + n], big[2, off:off + n]]
+    x2 = torch.zeros((3, n), dtype=torch.int32, device="cuda")
+    for i in range(3):
+        x2[i] = torch.from_numpy(c[i]).to(torch.int32)
+    big[1, (off + 1) % 4:(off + 1) % 4 + n] = x2[1]
+    out = torch.empty((3, L), dtype=torch.int32, device="cuda")
+    mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+    D.fused_conv(rows, gd, K, p.l, fl, None, True, L, n_in=n, out=out, mismatch=mm)
+    assert D.last_conv_kernel() == "tcgen05_m3"
+    assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref) and int(mm.item()) == 0
+
+
+def test_tcgen05_m3_envelope_by_sample_width(oracle):
+    """Samples wider than the m = 3 kernel's 2-byte planes (|c| > 0x7F7F)
+    need 5 digit planes: the flavour chosen from the data bound routes them
+    to the generic tcgen05 kernel, which stays exact."""
+    p = nent.derive_params(3, 48)
+    c = rand(9, (3, 9000), -40000, 40000)
+    g = rand(10, (64,), -100, 100)
+    ref = oracle.full_conv(c, g)
+    res = fused.entangled_conv(nent.StreamBlock(p, torch.from_numpy(c).cuda().to(torch.int32)), g,
+                               failed=None, out_dtype=torch.int32)
+    assert D.last_conv_kernel() in ("tcgen05", "mma.sync", "cuda-core")
+    assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), ref) and res.mismatches == 0
+    c2 = np.clip(c, -0x7F7F, 0x7F7F)
+    fl = imma_flavor(D.signed_digits(0x7F7F * ((1 << p.l) + 1)), 1)
+    res = fused.entangled_conv(nent.StreamBlock(p, torch.from_numpy(c2).cuda().to(torch.int32)), g,
+                               failed=0, flavor=fl, out_dtype=torch.int32)
+    assert D.last_conv_kernel() == "tcgen05_m3"
+    assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), oracle.full_conv(c2, g))

@@ -148,6 +148,158 @@ extract_kernel(const Rows delta, MutRows out, int m, int64_t n, int l, int r, in
   }
 }
 
+// ---------------------------------------------- vectorised K1 / K3 (16-byte) --
+// Four consecutive positions per thread and iteration, moved as 16-byte
+// vectors (one int4 of int32 words or two longlong2 of int64 words per row):
+// every row of the launch is 16-byte aligned at position `head` (0..3, found
+// on the host), positions outside [head, head + 4 nq) go through the scalar
+// path of block 0.  HBM-bound: several vectors per row in flight per thread.
+template <typename T>
+__device__ __forceinline__ void load4(const T* __restrict__ p, int64_t j, int64_t (&v)[4]) {
+  if (sizeof(T) == 4) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(p + j));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(p + j));
+    const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(p + j) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void store4(T* __restrict__ p, int64_t j, const int64_t (&v)[4]) {
+  if (sizeof(T) == 4) {
+    *reinterpret_cast<int4*>(p + j) = make_int4((int)(uint32_t)(uint64_t)v[0], (int)(uint32_t)(uint64_t)v[1],
+                                                (int)(uint32_t)(uint64_t)v[2], (int)(uint32_t)(uint64_t)v[3]);
+  } else {
+    reinterpret_cast<longlong2*>(p + j)[0] = make_longlong2(v[0], v[1]);
+    reinterpret_cast<longlong2*>(p + j)[1] = make_longlong2(v[2], v[3]);
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+entangle_vec_kernel(const Rows src, MutRows eps, int m, int64_t n, int64_t head, int64_t nq, int l, int64_t hi,
+                    int check, unsigned long long* bad) {
+  const int i = blockIdx.y;
+  const TI* __restrict__ cur = reinterpret_cast<const TI*>(src.p[i]);
+  const TI* __restrict__ prv = reinterpret_cast<const TI*>(src.p[(i + m - 1) % m]);
+  TO* __restrict__ out = reinterpret_cast<TO*>(eps.p[i]);
+  auto one = [&](int64_t j, int64_t a, int64_t b) {
+    if (check && wabs(b) > hi) atomicMin(bad, (unsigned long long)((int64_t)i * n + j));
+    return wadd(wshl(a, l), b);
+  };
+  constexpr int UV = 2;  // vectors per thread and iteration
+  const int64_t stride = (int64_t)gridDim.x * EW_THREADS * UV;
+  for (int64_t q0 = (int64_t)blockIdx.x * EW_THREADS * UV + threadIdx.x; q0 < nq; q0 += stride) {
+    int64_t a[UV][4], b[UV][4];
+#pragma unroll
+    for (int u = 0; u < UV; ++u) {
+      const int64_t q = q0 + (int64_t)u * EW_THREADS;
+      if (q < nq) {
+        load4(prv, head + 4 * q, a[u]);
+        load4(cur, head + 4 * q, b[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UV; ++u) {
+      const int64_t q = q0 + (int64_t)u * EW_THREADS;
+      if (q < nq) {
+        int64_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = one(head + 4 * q + k, a[u][k], b[u][k]);
+        store4(out, head + 4 * q, o);
+      }
+    }
+  }
+  if (blockIdx.x == 0) {  // the unaligned head and the ragged tail
+    for (int64_t j = threadIdx.x; j < n; j += EW_THREADS) {
+      if (j == head) j = head + 4 * nq;
+      if (j >= n) break;
+      out[j] = (TO)(uint64_t)one(j, (int64_t)__ldg(prv + j), (int64_t)__ldg(cur + j));
+    }
+  }
+}
+
+template <int MT, typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+extract_vec_kernel(const Rows delta, MutRows out, int64_t n, int64_t head, int64_t nq, int l, int r, int wide,
+                   unsigned long long* overflow, unsigned long long* mismatch) {
+  static_assert(MT > 0, "compile-time m");
+  auto pos = [&](int64_t j, const int64_t (&rot)[MT], int64_t (&orot)[MT]) {
+    const bool ovf = recover_rot<MT>(rot, MT, l, wide != 0, orot);
+    if (ovf && overflow) atomicAdd(overflow, 1ull);
+    if (mismatch) {
+      int64_t want = wadd(wshl(orot[MT - 1], l), orot[0]);
+      if (sizeof(TI) == 4) want = (int64_t)(int32_t)(uint32_t)(uint64_t)want;
+      if ((int64_t)__ldg(reinterpret_cast<const TI*>(delta.p[r]) + j) != want) atomicAdd(mismatch, 1ull);
+    }
+  };
+  const int64_t stride = (int64_t)gridDim.x * EW_THREADS;
+  for (int64_t q = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; q < nq; q += stride) {
+    const int64_t j = head + 4 * q;
+    int64_t in[MT - 1][4];
+#pragma unroll
+    for (int t = 0; t < MT - 1; ++t) {
+      int row = r + 1 + t;
+      row -= row >= MT ? MT : 0;
+      load4(reinterpret_cast<const TI*>(delta.p[row]), j, in[t]);
+    }
+    int64_t res[MT][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int64_t rot[MT], orot[MT];
+#pragma unroll
+      for (int t = 0; t < MT - 1; ++t) rot[t] = in[t][k];
+      rot[MT - 1] = 0;
+      pos(j + k, rot, orot);
+#pragma unroll
+      for (int t = 0; t < MT; ++t) res[t][k] = orot[t];
+    }
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      int row = r + t;
+      row -= row >= MT ? MT : 0;
+      store4(reinterpret_cast<TO*>(out.p[row]), j, res[t]);
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int64_t j = threadIdx.x; j < n; j += EW_THREADS) {
+      if (j == head) j = head + 4 * nq;
+      if (j >= n) break;
+      int64_t rot[MT], orot[MT];
+#pragma unroll
+      for (int t = 0; t < MT - 1; ++t) {
+        int row = r + 1 + t;
+        row -= row >= MT ? MT : 0;
+        rot[t] = (int64_t)__ldg(reinterpret_cast<const TI*>(delta.p[row]) + j);
+      }
+      rot[MT - 1] = 0;
+      pos(j, rot, orot);
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        int row = r + t;
+        row -= row >= MT ? MT : 0;
+        reinterpret_cast<TO*>(out.p[row])[j] = (TO)(uint64_t)orot[t];
+      }
+    }
+  }
+}
+
+// The position `head` in [0, 4) at which every row (element width `bits`) is
+// 16-byte aligned, or -1.
+static int64_t common_head(const void* const* rows, int k, int bits, const void* const* rows2, int k2,
+                           int bits2, int skip) {
+  for (int64_t h = 0; h < 4; ++h) {
+    bool ok = true;
+    for (int i = 0; i < k && ok; ++i)
+      if (i != skip && rows[i]) ok = ((reinterpret_cast<uintptr_t>(rows[i]) + h * (bits / 8)) & 15) == 0;
+    for (int i = 0; i < k2 && ok; ++i)
+      if (rows2[i]) ok = ((reinterpret_cast<uintptr_t>(rows2[i]) + h * (bits2 / 8)) & 15) == 0;
+    if (ok) return h;
+  }
+  return -1;
+}
+
 // Independent m=3 recipe (codec.py:151-183).
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(EW_THREADS)
@@ -303,6 +455,15 @@ int nent_entangle(const void* const* src, int src_bits, void* const* eps, int ep
   if (n == 0) return NENT_OK;
   Rows R = to_rows(src, m);
   MutRows W = to_mrows(eps, m);
+  const int64_t head = n >= 64 ? common_head(src, m, src_bits, eps, m, eps_bits, -1) : -1;
+  if (head >= 0) {  // 16-byte vectors
+    const int64_t nq = (n - head) / 4;
+    dim3 grid(grid_for(nq, EW_THREADS, 2, 148 * 16 / (m > 4 ? 4 : 1)), m);
+    DISPATCH_IO(src_bits, eps_bits,
+                (entangle_vec_kernel<TI, TO><<<grid, EW_THREADS, 0, s>>>(
+                    R, W, m, n, head, nq, l, check_hi, check, (unsigned long long*)bad_index_dev)));
+    return check_launch("entangle");
+  }
   dim3 grid(grid_for(n, EW_THREADS, EW_UNROLL, 148 * 16 / (m > 4 ? 4 : 1)), m);
   DISPATCH_IO(src_bits, eps_bits,
               (entangle_kernel<TI, TO><<<grid, EW_THREADS, 0, s>>>(
@@ -341,6 +502,25 @@ static int extract_impl(const void* const* delta, int delta_bits, void* const* o
     return NENT_ERR_PARAM;
   }
   MutRows O = to_mrows(out, m);
+  // 16-byte vectors when every row read (all but the failed one, plus the
+  // pivot when verifying) and every output row share an alignment phase
+  const int64_t head = (n >= 64 && (m == 3 || m == 4 || m == 8))
+                           ? common_head(D.p, m, delta_bits, O.p, m, out_bits, -1) : -1;
+  if (head >= 0) {
+    const int64_t nq = (n - head) / 4;
+    const int vgrid = grid_for(nq, EW_THREADS, 1, 148 * 8);
+#define EXTRACT_VEC_CASE(MTV)                                                                   \
+  DISPATCH_IO(delta_bits, out_bits,                                                             \
+              (extract_vec_kernel<MTV, TI, TO><<<vgrid, EW_THREADS, 0, s>>>(D, O, n, head, nq, l, r, wide, \
+                                                                           overflow_dev, mismatch_dev)))
+    switch (m) {
+      case 3: EXTRACT_VEC_CASE(3); break;
+      case 4: EXTRACT_VEC_CASE(4); break;
+      default: EXTRACT_VEC_CASE(8); break;
+    }
+#undef EXTRACT_VEC_CASE
+    return check_launch("extract");
+  }
   int grid = grid_for(n, EW_THREADS, 4);
 #define EXTRACT_CASE(MTV)                                                                  \
   DISPATCH_IO(delta_bits, out_bits,                                                        \

@@ -28,7 +28,7 @@
 //   warps 0-11  epilogue (3 per TMEM lane quadrant, 16 accumulator columns
 //               each; 128 registers after setmaxnreg)
 //   warps 12-18 producers: TMA bulk copies of the raw int32 windows into a
-//               3-deep staging ring, split into byte planes (2 tile slots)
+//               9-deep staging ring, split into byte planes (2 tile slots)
 //   warp 19     TMEM allocation; one elected lane issues every tcgen05.mma
 // TMEM: [0, 8*NG*NSTEPS) the Toeplitz tap digits (A operand), [192, 480) a
 // ring of 6 accumulator slots of 48 columns.
@@ -63,7 +63,8 @@ constexpr int PT = 32 * NPROD;         // producer threads
 constexpr int HALFW = 4;               // int4 words per producer thread and half window
 constexpr int NWP = 2 * HALFW * PT;    // int4 words staged per raw stream and tile (1792)
 constexpr uint32_t HALFB = HALFW * PT * 16;  // bytes per staging unit (14,336)
-constexpr int NSTAGE = 3;              // staging ring depth (TMA runs two units ahead)
+constexpr int NSTAGE = 9;              // staging ring depth: TMA runs 8 units (1.3 tiles) ahead,
+                                       // ~115 KB in flight per SM to cover HBM latency
 constexpr int PLANE = 7168;            // bytes per byte plane: >= 4 * NWP, 1024-aligned
 constexpr int SLOTB = 6 * PLANE;       // one tile slot: 3 raw streams x {lo, hi}
 constexpr int TAPCOLS = 192;
@@ -76,7 +77,8 @@ static_assert(NEPI % 4 == 0 && (NPROD + 1) % 4 == 0, "setmaxnreg acts on whole w
 static_assert(4 * NWP >= TILE + 256, "a staged window covers the tile plus the K <= 257 halo");
 static_assert(4 * NWP <= PLANE, "a staged window fits its plane");
 constexpr uint32_t SSTR = HALFB + 128;  // staging slot stride: a unit plus one int4 of lead-in
-constexpr size_t SMEM = 2 * (size_t)SLOTB + NSTAGE * (size_t)SSTR;  // 129,408 B
+constexpr size_t SMEM = 2 * (size_t)SLOTB + NSTAGE * (size_t)SSTR;  // 216,192 B
+static_assert(SMEM + 1024 <= 227 * 1024, "shared memory");
 
 struct Geom {
   int KT, nsteps;

@@ -515,3 +515,41 @@ def test_tcgen05_m3_envelope_by_sample_width(oracle):
                                failed=0, flavor=fl, out_dtype=torch.int32)
     assert D.last_conv_kernel() == "tcgen05_m3"
     assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), oracle.full_conv(c2, g))
+
+
+@pytest.mark.parametrize("m,w", [(3, 32), (3, 48), (3, 64), (4, 64), (5, 32), (8, 32)])
+@pytest.mark.parametrize("n,off", [(7, 0), (63, 1), (1000, 0), (1001, 3), (4099, 2), (1 << 16, 0)])
+def test_k1_k3_vectorised_and_scalar_paths(oracle, m, w, n, off):
+    """K1 (entangle) and K3 (extract, every failed index, and the verifying
+    form) against the oracle at every row phase: rows sliced `off` words into
+    their buffers take the 16-byte vector path from the first aligned
+    position (scalar head / tail), short rows the scalar kernel."""
+    p = nent.derive_params(m, w)
+    hi = nent.input_range(p).hi
+    c = rand(n * m + w + off, (m, n), -min(hi, 1 << 30), min(hi, 1 << 30))
+    eps_ref = oracle.entangle(c, p.l)
+    for dt in ((torch.int64,) if w > 32 else (torch.int32, torch.int64)):
+        big = torch.zeros((m, n + 8), dtype=dt, device="cuda")
+        big[:, off:off + n] = torch.from_numpy(c).to(dt)
+        x = big[:, off:off + n]
+        ebig = torch.zeros((m, n + 8), dtype=torch.int64, device="cuda")
+        eps = ebig[:, off:off + n]
+        D.entangle(x, p.l, out_dtype=torch.int64, out=eps)
+        assert np.array_equal(eps.cpu().numpy(), eps_ref), (m, w, n, off, dt)
+    ebig = torch.zeros((m, n + 8), dtype=torch.int64, device="cuda")
+    ebig[:, off:off + n] = torch.from_numpy(eps_ref)
+    delta = ebig[:, off:off + n]
+    for out_dt in (torch.int32, torch.int64):
+        obig = torch.zeros((m, n + 8), dtype=out_dt, device="cuda")
+        out = obig[:, off:off + n]
+        for r in range(m):
+            D.extract(delta, m, p.l, r, wide=w > 32, out=out, check_overflow=False)
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), c), (m, w, n, off, r, out_dt)
+        mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+        D.extract_verify(delta, m, p.l, 0, w > 32, mm, out=out)
+        assert int(mm.item()) == 0 and np.array_equal(out.to(torch.int64).cpu().numpy(), c)
+    bad = delta.clone()
+    bad[0, n // 2] += 1  # an inconsistent redundant word is counted
+    mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+    D.extract_verify(bad, m, p.l, 0, w > 32, mm)
+    assert int(mm.item()) == 1

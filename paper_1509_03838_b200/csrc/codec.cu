@@ -211,10 +211,10 @@ entangle_vec_kernel(const Rows src, MutRows eps, int m, int64_t n, int64_t head,
       }
     }
   }
-  if (blockIdx.x == 0) {  // the unaligned head and the ragged tail
-    for (int64_t j = threadIdx.x; j < n; j += EW_THREADS) {
-      if (j == head) j = head + 4 * nq;
-      if (j >= n) break;
+  if (blockIdx.x == 0) {  // the unaligned head [0, head) and the ragged tail [head + 4 nq, n)
+    const int64_t tail0 = head + 4 * nq, ns = head + (n - tail0);
+    for (int64_t k = threadIdx.x; k < ns; k += EW_THREADS) {
+      const int64_t j = k < head ? k : tail0 + (k - head);
       out[j] = (TO)(uint64_t)one(j, (int64_t)__ldg(prv + j), (int64_t)__ldg(cur + j));
     }
   }
@@ -262,10 +262,10 @@ extract_vec_kernel(const Rows delta, MutRows out, int64_t n, int64_t head, int64
       store4(reinterpret_cast<TO*>(out.p[row]), j, res[t]);
     }
   }
-  if (blockIdx.x == 0) {
-    for (int64_t j = threadIdx.x; j < n; j += EW_THREADS) {
-      if (j == head) j = head + 4 * nq;
-      if (j >= n) break;
+  if (blockIdx.x == 0) {  // the unaligned head [0, head) and the ragged tail [head + 4 nq, n)
+    const int64_t tail0 = head + 4 * nq, ns = head + (n - tail0);
+    for (int64_t k = threadIdx.x; k < ns; k += EW_THREADS) {
+      const int64_t j = k < head ? k : tail0 + (k - head);
       int64_t rot[MT], orot[MT];
 #pragma unroll
       for (int t = 0; t < MT - 1; ++t) {

@@ -3,6 +3,7 @@
 // envelope return NENT_TC05_NA and take the generic tcgen05 kernel.
 #include "conv_tc05_m3.cuh"
 
+#include <cstdio>
 #include <cstdlib>
 
 namespace nent {
@@ -60,8 +61,30 @@ int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
   if (!kern) return NENT_TC05_NA;
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
+#ifdef NENT_TC05_TIMERS
+  static unsigned long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, 64 * sizeof(unsigned long long));
+  cudaMemsetAsync(dbg, 0, 64 * sizeof(unsigned long long), s);
+  G.dbg = dbg;
+#endif
   kern<<<grid, NT, SMEM, s>>>(A, G);
   note_conv_kernel(4);
+#ifdef NENT_TC05_TIMERS
+  {
+    unsigned long long h[64];
+    cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "m3 timers (kcycles/CTA): mma wait_full %.1f wait_acce %.1f total %.1f | epi wait_accf %.1f total %.1f"
+            " | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid, h[6] / 1e3 / grid,
+            h[8] / 1e3 / grid, (double)G.ntiles / grid);
+    for (int w = 0; w < 2; ++w) {
+      const unsigned long long* q = h + 16 + 8 * w;
+      fprintf(stderr, "  producer warp %d: wait_empty %.1f wait_tma %.1f issue+sync %.1f load %.1f convert+sts %.1f "
+              "tail %.1f total %.1f\n", w, q[0] / 1e3 / grid, q[1] / 1e3 / grid, q[2] / 1e3 / grid, q[3] / 1e3 / grid,
+              q[4] / 1e3 / grid, q[5] / 1e3 / grid, q[6] / 1e3 / grid);
+    }
+  }
+#endif
   return check_launch("tc05 fused m3");
 }
 

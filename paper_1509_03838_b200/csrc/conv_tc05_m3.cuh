@@ -63,21 +63,32 @@ constexpr int PT = 32 * NPROD;         // producer threads
 constexpr int HALFW = 4;               // int4 words per producer thread and half window
 constexpr int NWP = 2 * HALFW * PT;    // int4 words staged per raw stream and tile (1792)
 constexpr uint32_t HALFB = HALFW * PT * 16;  // bytes per staging unit (14,336)
-constexpr int NSTAGE = 9;              // staging ring depth: TMA runs 8 units (1.3 tiles) ahead,
-                                       // ~115 KB in flight per SM to cover HBM latency
+#ifndef NENT_M3_NSTAGE
+#define NENT_M3_NSTAGE 4
+#endif
+#ifndef NENT_M3_NSLOT
+#define NENT_M3_NSLOT 2
+#endif
+constexpr int NSLOT = NENT_M3_NSLOT;   // tile slots of byte planes: producers run up to NSLOT-1 tiles ahead
+// Each producer warp owns a contiguous 1/NPROD of every
+// raw stream's window (WW int4 per lane, 4 KB per warp) and stages it through
+// its own TMA ring of NSTAGE chunks: the warps never wait for each other.
+constexpr int NSTAGE = NENT_M3_NSTAGE;  // per-warp staging ring depth (NSTAGE-1 units in flight)
+constexpr int WW = 2 * HALFW;           // int4 words per lane and raw-stream window (8)
+constexpr uint32_t WCHUNK = WW * 32 * 16;  // bytes per warp and unit (4096)
 constexpr int PLANE = 7168;            // bytes per byte plane: >= 4 * NWP, 1024-aligned
 constexpr int SLOTB = 6 * PLANE;       // one tile slot: 3 raw streams x {lo, hi}
 constexpr int TAPCOLS = 192;
 constexpr int RING0 = TAPCOLS;
 constexpr int SLOTS = (512 - RING0) / U;  // 6
 constexpr int LAUNCH_REGS = 96;        // 65536 / 640 rounded down to 8
-constexpr int EPI_REGS = 128, PROD_REGS = 48;
+constexpr int EPI_REGS = 112, PROD_REGS = 72;
 static_assert(NEPI * 32 * EPI_REGS + (NPROD + 1) * 32 * PROD_REGS <= NT * LAUNCH_REGS, "launch register pool");
 static_assert(NEPI % 4 == 0 && (NPROD + 1) % 4 == 0, "setmaxnreg acts on whole warpgroups");
 static_assert(4 * NWP >= TILE + 256, "a staged window covers the tile plus the K <= 257 halo");
 static_assert(4 * NWP <= PLANE, "a staged window fits its plane");
-constexpr uint32_t SSTR = HALFB + 128;  // staging slot stride: a unit plus one int4 of lead-in
-constexpr size_t SMEM = 2 * (size_t)SLOTB + NSTAGE * (size_t)SSTR;  // 216,192 B
+constexpr uint32_t SSTR = WCHUNK + 128;  // staging slot stride: a chunk plus one int4 of lead-in
+constexpr size_t SMEM = NSLOT * (size_t)SLOTB + (size_t)NPROD * NSTAGE * SSTR;  // 204,288 B
 static_assert(SMEM + 1024 <= 227 * 1024, "shared memory");
 
 struct Geom {
@@ -86,7 +97,21 @@ struct Geom {
   int shift;   // tiles start `shift` outputs early: row 0's windows are 16-byte aligned
   int dph[3];  // word phase of row s relative to row 0 (mod 4): its windows are
                // copied from dph[s] words earlier and read shifted in shared memory
+  unsigned long long* dbg;  // role timers (profiling builds, -DNENT_TC05_TIMERS)
 };
+
+// TM(slot, stmt): add stmt's cycles to tw[slot] in timer builds
+#ifdef NENT_TC05_TIMERS
+#define TM(i, ...)                    \
+  {                                   \
+    const long long t0_ = clock64();  \
+    __VA_ARGS__;                      \
+    tw[i] += clock64() - t0_;         \
+  }
+#else
+#define TM(i, ...) \
+  { __VA_ARGS__; }
+#endif
 
 // u = c + 0x8080 of 4 consecutive samples -> the lo-byte and hi-byte plane words
 __device__ __forceinline__ void split2(int4 v, uint32_t& lo, uint32_t& hi) {
@@ -104,6 +129,42 @@ __device__ __forceinline__ void split2(int4 v, uint32_t& lo, uint32_t& hi) {
 __device__ __forceinline__ void pin(uint64_t& x) { asm volatile("" : "+l"(x)); }
 __device__ __forceinline__ void pin(uint32_t& x) { asm volatile("" : "+r"(x)); }
 
+// acc += (int64)r * 2^(8c + s0) (mod 2^64) with a compile-time weight: one
+// IMAD.WIDE for weights < 2^31, one IMAD on the high word otherwise
+template <int SH>
+__device__ __forceinline__ void add_shifted(uint64_t& acc, uint32_t r) {
+  if (SH < 31) {
+    acc += (uint64_t)((int64_t)(int32_t)r * (int64_t)(1ll << SH));
+  } else {
+    acc += (uint64_t)(r << (SH - 32)) << 32;
+  }
+}
+template <int SH>
+__device__ __forceinline__ void sub_shifted(uint64_t& acc, uint32_t r) {
+  if (SH < 31) {
+    acc += (uint64_t)((int64_t)(int32_t)r * -(int64_t)(1ll << SH));
+  } else {
+    acc -= (uint64_t)(r << (SH - 32)) << 32;
+  }
+}
+// class c of delta_A and delta_B into C = (delta_A << 16) - delta_B and the
+// low word of delta_A
+template <int CL, int N>
+__device__ __forceinline__ void fold_ab(uint64_t (&C)[N], uint32_t (&lowA)[N], const uint32_t (&rA)[N],
+                                        const uint32_t (&rB)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    add_shifted<8 * CL + 16>(C[i], rA[i]);
+    sub_shifted<8 * CL>(C[i], rB[i]);
+    if (CL < 4) lowA[i] += rA[i] << (8 * CL);
+  }
+}
+template <int CL, int N>
+__device__ __forceinline__ void fold_p(uint64_t (&acc)[N], const uint32_t (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) add_shifted<8 * CL>(acc[i], r[i]);
+}
+
 // the chains (data digit p, tap digit j) of digit class c, in a fixed order
 template <int NG, typename F>
 __device__ __forceinline__ void for_class(int c, F&& f) {
@@ -120,28 +181,25 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
   constexpr int NCLS = 4 + NG - 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // full[2], empty[2], stage full[3], stage empty[3], acc full[5], acc empty[5]
-  __shared__ __align__(8) uint64_t bars[4 + 2 * NSTAGE + 2 * SLOTS];
+  __shared__ __align__(8) uint64_t bars[2 * NSLOT + NPROD * NSTAGE + 2 * SLOTS];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t planes_s = tc05::smem_u32(smem_raw);
-  const uint32_t stage_s = planes_s + 2u * SLOTB;
+  const uint32_t stage_s = planes_s + (uint32_t)(NSLOT * SLOTB);
   const uint32_t bar0 = tc05::smem_u32(bars);
   auto full_b = [&](int s) { return bar0 + 8u * (uint32_t)s; };
-  auto empty_b = [&](int s) { return bar0 + 8u * (uint32_t)(2 + s); };
-  auto stg_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + s); };
-  auto stge_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + NSTAGE + s); };
-  auto accf_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + 2 * NSTAGE + s); };
-  auto acce_b = [&](int s) { return bar0 + 8u * (uint32_t)(4 + 2 * NSTAGE + SLOTS + s); };
+  auto empty_b = [&](int s) { return bar0 + 8u * (uint32_t)(NSLOT + s); };
+  constexpr int B0 = 2 * NSLOT;
+  auto stg_b = [&](int w, int s) { return bar0 + 8u * (uint32_t)(B0 + w * NSTAGE + s); };  // warp w's ring
+  auto accf_b = [&](int s) { return bar0 + 8u * (uint32_t)(B0 + NPROD * NSTAGE + s); };
+  auto acce_b = [&](int s) { return bar0 + 8u * (uint32_t)(B0 + NPROD * NSTAGE + SLOTS + s); };
 
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mb_init(full_b(s), PT);
+    for (int s = 0; s < NSLOT; ++s) {
+      mb_init(full_b(s), NPROD);  // one arrival per producer warp and tile
       mb_init(empty_b(s), 1);
     }
-    for (int s = 0; s < NSTAGE; ++s) {
-      mb_init(stg_b(s), 1);
-      mb_init(stge_b(s), PT);
-    }
+    for (int s = 0; s < NPROD * NSTAGE; ++s) mb_init(stg_b(0, s), 1);
     for (int s = 0; s < SLOTS; ++s) {
       mb_init(accf_b(s), 1);
       mb_init(acce_b(s), NEPI);
@@ -158,7 +216,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     // the reversed taps' digits, staged once in the (still free) staging ring:
     // rev[j][i] = digit_j(g[KT-1-i]), A_j[v][k] = rev[j][k - v + 127]
     const int RL = G.KT + 128;
-    unsigned char* rev = smem_raw + 2 * SLOTB;
+    unsigned char* rev = smem_raw + NSLOT * SLOTB;
     const uint64_t gbias = bias_of(NG);
     for (int i = tid; i < RL; i += NT) {
       const int idx = G.KT - 1 - i;
@@ -187,6 +245,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
   const int P = verify ? 0 : A.r;  // pivot: the stream never read (or checked last)
   const int sA = P + 1 >= 3 ? P - 2 : P + 1, sB = P + 2 >= 3 ? P - 1 : P + 2;
   const int64_t my_tiles = G.ntiles > blockIdx.x ? (G.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  long long tw[6] = {0, 0, 0, 0, 0, 0};
+  const long long tstart = clock64();
 
   if (warp < NEPI) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
@@ -202,22 +262,28 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     const uint64_t corr = 0 - 128 * gsum * 0x01010101ull;
     unsigned bad = 0;
     int kslot = 0;  // running accumulator-slot use (same sequence as the MMA warp)
-    // TMEM -> registers for the next ring slot, which is then handed back to
-    // the MMA warp
-    auto drain = [&](uint32_t (&r)[EC]) {
-      const int rs = kslot % SLOTS;
-      mb_wait_sleep(accf_b(rs), (uint32_t)((kslot / SLOTS) & 1));
-      tc05::fence_after();
-#ifndef NENT_M3_DBG_NOLD
-      tc05::ld_x16(tbase + lrow + (uint32_t)(RING0 + rs * U + EC * part), r);
+    // TMEM -> registers for the next one or two ring slots (one TMEM round
+    // trip: both loads, one wait), which are then handed back to the MMA warp
+    auto drain2 = [&](uint32_t (&ra)[EC], uint32_t (&rb)[EC], bool two) {
+      const int r0 = kslot % SLOTS, r1 = (kslot + 1) % SLOTS;
+#ifdef NENT_M3_EPI_SPIN
+      TM(0, mb_wait(accf_b(r0), (uint32_t)((kslot / SLOTS) & 1)));
+      if (two) TM(0, mb_wait(accf_b(r1), (uint32_t)(((kslot + 1) / SLOTS) & 1)));
 #else
-      for (int i = 0; i < EC; ++i) r[i] = 0;
+      TM(0, mb_wait_sleep(accf_b(r0), (uint32_t)((kslot / SLOTS) & 1)));
+      if (two) TM(0, mb_wait_sleep(accf_b(r1), (uint32_t)(((kslot + 1) / SLOTS) & 1)));
 #endif
+      tc05::fence_after();
+      tc05::ld_x16(tbase + lrow + (uint32_t)(RING0 + r0 * U + EC * part), ra);
+      if (two) tc05::ld_x16(tbase + lrow + (uint32_t)(RING0 + r1 * U + EC * part), rb);
       tc05::wait_ld();
       tc05::fence_before();
       __syncwarp();
-      if (lane == 0) mb_arrive(acce_b(rs));
-      ++kslot;
+      if (lane == 0) {
+        mb_arrive(acce_b(r0));
+        if (two) mb_arrive(acce_b(r1));
+      }
+      kslot += two ? 2 : 1;
     };
     int32_t* yP = reinterpret_cast<int32_t*>(A.y.p[P]);
     int32_t* yA = reinterpret_cast<int32_t*>(A.y.p[sA]);
@@ -235,7 +301,9 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       //   d_{P+2} = -sext32(C),  d_P = hi32(C) - (C_lo < 0),
       //   d_{P+1} = delta_A - (d_P << 16)                          (mod 2^32)
       // so each output keeps one 64-bit and one 32-bit accumulator, folded
-      // class by class straight out of TMEM (class c carries weight 256^c).
+      // class by class straight out of TMEM (class c carries weight 256^c,
+      // an immediate: the class loop is unrolled).  The MMA warp issues class
+      // c of A and of B into consecutive slots: one drain per class.
       uint64_t C[EC];
       uint32_t lowA[EC];
 #pragma unroll
@@ -243,22 +311,21 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         C[i] = (corr << 16) - corr;
         lowA[i] = (uint32_t)corr;
       }
-      // a rolled class loop: the next class's TMEM load is not hoisted above
-      // this class's fold (which would keep extra registers live and spill)
+      // A rolled class loop (ptxas would otherwise sink each class's fold below
+      // the next classes' TMEM loads and spill the extra live registers) whose
+      // body switches to a fold with compile-time class weights: every term is
+      // one IMAD.WIDE (or one IMAD on the high word for weights >= 2^32).
 #pragma unroll 1
       for (int c = 0; c < NCLS; ++c) {
-        uint32_t r[EC];
-        const int sh = 8 * c;
-        drain(r);  // class c of delta_A
-#pragma unroll
-        for (int i = 0; i < EC; ++i) {
-          const int64_t ra = (int64_t)(int32_t)r[i];
-          C[i] += (uint64_t)ra << (sh + 16);
-          lowA[i] += r[i] << sh;  // c = 4 adds r << 32 = 0 (mod 2^32)
+        uint32_t rA[EC], rB[EC];
+        drain2(rA, rB, true);
+        switch (c) {
+          case 0: fold_ab<0>(C, lowA, rA, rB); break;
+          case 1: fold_ab<1>(C, lowA, rA, rB); break;
+          case 2: fold_ab<2>(C, lowA, rA, rB); break;
+          case 3: fold_ab<3>(C, lowA, rA, rB); break;
+          default: fold_ab<4>(C, lowA, rA, rB); break;
         }
-        drain(r);  // class c of delta_B
-#pragma unroll
-        for (int i = 0; i < EC; ++i) C[i] -= (uint64_t)(int64_t)(int32_t)r[i] << sh;
       }
       uint64_t accP[EC];
 #pragma unroll
@@ -267,18 +334,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         const int32_t d0 = (int32_t)(uint32_t)(C[i] >> 32) - (vv >> 31);
         const int32_t d1 = (int32_t)(lowA[i] - ((uint32_t)d0 << 16));
         const int64_t o = o0 + 128 * i;
-#ifdef NENT_M3_DBG_NOSTORE
-        if (false) {
-#else
         if (interior || (o >= 0 && o < A.n_out)) {
-#endif
-#ifdef NENT_M3_CHECK
-          if (o < 0 || o >= A.n_out) {
-            printf("M3CHECK store cta %d tile %lld o %lld n_out %lld\n", blockIdx.x, (long long)tile, (long long)o,
-                   (long long)A.n_out);
-            __trap();
-          }
-#endif
           yP[o] = d0;
           yA[o] = d1;
           yB[o] = (int32_t)(0u - (uint32_t)vv);
@@ -287,13 +343,17 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         // (d_{P+2} << 16) + d_P: start its fold at minus that
         accP[i] = corr - ((uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << 16));
       }
-      if (verify) {
+      if (verify) {  // the redundant stream P, two classes per drain
 #pragma unroll 1
-        for (int c = 0; c < NCLS; ++c) {
-          uint32_t r[EC];
-          drain(r);
-#pragma unroll
-          for (int i = 0; i < EC; ++i) accP[i] += (uint64_t)(int64_t)(int32_t)r[i] << (8 * c);
+        for (int c = 0; c < NCLS; c += 2) {
+          uint32_t r0[EC], r1[EC];
+          const bool two = c + 1 < NCLS;
+          drain2(r0, r1, two);
+          switch (c) {
+            case 0: fold_p<0>(accP, r0); fold_p<1>(accP, r1); break;
+            case 2: fold_p<2>(accP, r0); if (two) fold_p<3>(accP, r1); break;
+            default: fold_p<4>(accP, r0); break;
+          }
         }
 #pragma unroll
         for (int i = 0; i < EC; ++i) {
@@ -314,8 +374,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       const uint32_t idesc = tc05::idesc_i8(128, U, /*b_signed=*/false);
       int kslot = 0;
       for (int64_t t = 0; t < my_tiles; ++t) {
-        const int ts = (int)(t & 1);
-        mb_wait(full_b(ts), (uint32_t)((t >> 1) & 1));
+        const int ts = (int)(t % NSLOT);
+        TM(0, mb_wait(full_b(ts), (uint32_t)((t / NSLOT) & 1)));
         tc05::fence_after();
         if (elect_one()) {
           const uint32_t slot_s = planes_s + (uint32_t)(ts * SLOTB);
@@ -323,7 +383,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
           auto issue_class = [&](int i, int c) {
             const int rs = kslot % SLOTS, use = kslot / SLOTS;
             if (use >= 1) {
-              mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1));
+              TM(1, mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1)));
               tc05::fence_after();
             }
             const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
@@ -359,106 +419,145 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       }
       // drain the last tiles' commits before the CTA can exit: an mbarrier
       // arrive still in flight must not land in a successor CTA's shared memory
-      for (int64_t t = my_tiles > 2 ? my_tiles - 2 : 0; t < my_tiles; ++t)
-        mb_wait(empty_b((int)(t & 1)), (uint32_t)((t >> 1) & 1));
+      for (int64_t t = my_tiles > NSLOT ? my_tiles - NSLOT : 0; t < my_tiles; ++t)
+        mb_wait(empty_b((int)(t % NSLOT)), (uint32_t)((t / NSLOT) & 1));
     } else {
       // ---------------- producers ----------------
-      const int ptid = tid - 32 * NEPI;  // 0 .. PT-1
-      const int64_t units = my_tiles * 6;
-      // unit H: tile t = H / 6, raw stream s = (H % 6) / 2, half h = H % 2.
-      // mode 1: the window is inside [0, n_in) -> TMA bulk copy into the ring;
-      // mode 2: per-thread loads with zero padding outside [0, n_in)
-      auto unit_P0 = [&](int64_t H) {
-        const int64_t tile = blockIdx.x + (H / 6) * gridDim.x;
-        return A.y_begin - G.shift + tile * TILE - (G.KT - 128);
-      };
-      auto unit_mode = [&](int64_t H) {
-        const int64_t P0 = unit_P0(H);
-#ifdef NENT_M3_DBG_NOTMA
-        return 2;
-#endif
+      const int pw = warp - NEPI;  // producer warp 0 .. NPROD-1
+      // Units in order: tile t (the CTA's t-th), raw stream s.  Warp pw owns
+      // int4 words [pw*WW*32, (pw+1)*WW*32) of every raw stream's window,
+      // lane-consecutive (word pw*WW*32 + 32i + lane, i < WW).  mode 1 (the
+      // tile's windows inside [0, n_in)): one TMA bulk copy of the warp's
+      // 4 KB chunk into its own ring; mode 2: per-lane loads, zero padding.
+      const int64_t P0_first = A.y_begin - G.shift + (int64_t)blockIdx.x * TILE - (G.KT - 128);
+      const int64_t P0_step = (int64_t)gridDim.x * TILE;
+      const uint32_t ring = stage_s + (uint32_t)(pw * NSTAGE) * SSTR;
+      const int wbase = pw * WW * 32;
+      // per-stream operands by select (a runtime-indexed array would live in local memory)
+      const int dph0 = G.dph[0], dph1 = G.dph[1], dph2 = G.dph[2];
+      const int32_t* row0 = reinterpret_cast<const int32_t*>(A.b.p[0]);
+      const int32_t* row1 = reinterpret_cast<const int32_t*>(A.b.p[1]);
+      const int32_t* row2 = reinterpret_cast<const int32_t*>(A.b.p[2]);
+      auto dph_of = [&](int k) { return k == 0 ? dph0 : (k == 1 ? dph1 : dph2); };
+      auto row_of = [&](int k) { return k == 0 ? row0 : (k == 1 ? row1 : row2); };
+      // swizzled plane offset of this lane's word i
+      auto soff = [&](int i) { return tc05::sw128(4u * (uint32_t)(wbase + 32 * i + lane)); };
+      auto mode_of = [&](int64_t P0) {
         return (P0 >= 4 && P0 + 4 * (int64_t)NWP + 4 <= A.n_in) ? 1 : 2;
       };
-      // TMA issue (thread 0): units up to H + NSTAGE - 1, mode-1 units only,
-      // each into ring buffer (j % NSTAGE) for the j-th mode-1 unit
-      int64_t next_issue = 0, issued = 0, consumed = 0;
-      auto issue_upto = [&](int64_t Hmax) {
-        for (; next_issue < units && next_issue <= Hmax; ++next_issue) {
-          if (unit_mode(next_issue) != 1) continue;
-          const int b = (int)(issued % NSTAGE);
-          if (issued >= NSTAGE) mb_wait(stge_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1));
-          const int s = (int)((next_issue % 6) / 2), h = (int)(next_issue & 1);
-          const int d = G.dph[s];
-          const char* src = reinterpret_cast<const char*>(reinterpret_cast<const int32_t*>(A.b.p[s]) +
-                                                          unit_P0(next_issue) - d) + (size_t)h * HALFB;
-          const uint32_t bytes = HALFB + (d ? 16u : 0u);
-#ifdef NENT_M3_CHECK
-          if ((reinterpret_cast<uintptr_t>(src) & 15) || ((stage_s + (uint32_t)b * SSTR) & 15) || (bytes & 15) ||
-              unit_P0(next_issue) - d < 0 || unit_P0(next_issue) - d + (int64_t)h * HALFB / 4 + bytes / 4 > A.n_in) {
-            printf("M3CHECK tma cta %d unit %lld s %d h %d P0 %lld d %d src %p bytes %u n_in %lld\n", blockIdx.x,
-                   (long long)next_issue, s, h, (long long)unit_P0(next_issue), d, src, bytes, (long long)A.n_in);
-            __trap();
+      const int units = (int)my_tiles * 3;
+      // TMA issue cursor (lane 0)
+      int64_t iP0 = P0_first;
+      int n_issue = 0, is = 0, imode = mode_of(P0_first);
+      int issued = 0, consumed = 0;
+      auto issue_upto = [&](int Hmax) {
+        for (; n_issue < units && n_issue <= Hmax; ++n_issue) {
+          if (imode == 1) {
+            const int b = issued % NSTAGE;  // free: this warp consumed it NSTAGE issues ago
+            const int d = dph_of(is);
+            const char* src = reinterpret_cast<const char*>(row_of(is) + iP0 - d) + (size_t)wbase * 16;
+            const uint32_t bytes = WCHUNK + (d ? 16u : 0u);
+            mb_expect_tx(stg_b(pw, b), bytes);
+            bulk_g2s(ring + (uint32_t)b * SSTR, src, bytes, stg_b(pw, b));
+            ++issued;
           }
-#endif
-          mb_expect_tx(stg_b(b), bytes);
-          bulk_g2s(stage_s + (uint32_t)b * SSTR, src, bytes, stg_b(b));
-          ++issued;
+          if (++is == 3) {
+            is = 0;
+            iP0 += P0_step;
+            imode = mode_of(iP0);
+          }
         }
       };
-      for (int64_t H = 0; H < units; ++H) {
-        const int64_t t = H / 6;
-        const int ts = (int)(t & 1);
-        const int s = (int)((H % 6) / 2), h = (int)(H & 1);
-        if (H % 6 == 0 && t >= 2) mb_wait_sleep(empty_b(ts), (uint32_t)(((t >> 1) - 1) & 1));
-        if (ptid == 0) issue_upto(H + NSTAGE - 1);
+      int64_t P0 = P0_first;
+      int t = 0, s = 0, mode = mode_of(P0_first);
+      for (int H = 0; H < units; ++H) {
+        const int ts = (int)(t % NSLOT);
+        // the previous unit's staging reads are complete (converted and
+        // stored): lane 0 may refill that buffer
+        __syncwarp();
+        if (lane == 0) TM(2, issue_upto(H + NSTAGE - 1));
+        if (s == 0 && t >= NSLOT) TM(0, mb_wait_sleep(empty_b(ts), (uint32_t)(((t / NSLOT) - 1) & 1)));
         const uint32_t plo = planes_s + (uint32_t)(ts * SLOTB + (2 * s) * PLANE);
-        int4 v[HALFW];
-        if (unit_mode(H) == 1) {
-          const int b = (int)(consumed % NSTAGE);
-          mb_wait_sleep(stg_b(b), (uint32_t)((consumed / NSTAGE) & 1));
-          const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
-          const int d = G.dph[s];
-          if (d == 0) {
-            const int4* sb = reinterpret_cast<const int4*>(__cvta_shared_to_generic(sbuf));
+        if (mode == 1) {
+          const int b = consumed % NSTAGE;
+          TM(1, mb_wait_sleep(stg_b(pw, b), (uint32_t)((consumed / NSTAGE) & 1)));
+          const uint32_t sbuf = ring + (uint32_t)b * SSTR;
+          const int d = dph_of(s);
+          TM(4, {
 #pragma unroll
-            for (int i = 0; i < HALFW; ++i) v[i] = sb[i * PT + ptid];
-          } else {  // this row's window starts d words into the staged copy
-            const uint32_t* sw = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d;
+          for (int i0 = 0; i0 < WW; i0 += 4) {
+            int4 v[4];
+            if (d == 0) {
+              const int4* sb = reinterpret_cast<const int4*>(__cvta_shared_to_generic(sbuf));
 #pragma unroll
-            for (int i = 0; i < HALFW; ++i) {
-              const uint32_t* q = sw + 4 * (i * PT + ptid);
-              v[i] = make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]);
+              for (int i = 0; i < 4; ++i) v[i] = sb[(i0 + i) * 32 + lane];
+            } else {  // this row's window starts d words into the staged copy
+              const uint32_t* sw = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t* q = sw + 4 * ((i0 + i) * 32 + lane);
+                v[i] = make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint32_t lo, hi;
+              split2(v[i], lo, hi);
+              const uint32_t off = soff(i0 + i);
+              sts32(plo + off, lo);
+              sts32(plo + (uint32_t)PLANE + off, hi);
             }
           }
-          mb_arrive(stge_b(b));  // this thread is done with the buffer
+          });
           ++consumed;
         } else {
-          const int32_t* bp = reinterpret_cast<const int32_t*>(A.b.p[s]);
-          const int64_t P0 = unit_P0(H);
+          const int32_t* bp = row_of(s);
 #pragma unroll
-          for (int i = 0; i < HALFW; ++i) {
-            const int64_t q0 = P0 + 4 * (int64_t)(ptid + PT * (HALFW * h + i));
+          for (int i = 0; i < WW; ++i) {
+            const int64_t q0 = P0 + 4 * (int64_t)(wbase + 32 * i + lane);
             int e[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) e[k] = (q0 + k >= 0 && q0 + k < A.n_in) ? __ldg(bp + q0 + k) : 0;
-            v[i] = make_int4(e[0], e[1], e[2], e[3]);
+            uint32_t lo, hi;
+            split2(make_int4(e[0], e[1], e[2], e[3]), lo, hi);
+            const uint32_t off = soff(i);
+            sts32(plo + off, lo);
+            sts32(plo + (uint32_t)PLANE + off, hi);
           }
         }
-#pragma unroll
-        for (int i = 0; i < HALFW; ++i) {
-          uint32_t lo, hi;
-          split2(v[i], lo, hi);
-          const uint32_t off = tc05::sw128(4u * (uint32_t)(ptid + PT * (HALFW * h + i)));
-          sts32(plo + off, lo);
-          sts32(plo + (uint32_t)PLANE + off, hi);
+        if (s == 2) {  // the tile's planes are complete (this warp's share)
+          TM(5, {
+          fence_async_smem();  // this thread's plane writes -> the MMA's async-proxy reads
+          __syncwarp();
+          if (lane == 0) mb_arrive(full_b(ts));
+          });
         }
-        if (H % 6 == 5) {
-          fence_async_smem();
-          mb_arrive(full_b(ts));
+        if (++s == 3) {
+          s = 0;
+          ++t;
+          P0 += P0_step;
+          mode = mode_of(P0);
         }
       }
     }
   }
+#ifdef NENT_TC05_TIMERS
+  // role timers: [mma wait_full, wait_acce, total | prod wait_empty, wait_tma,
+  // total | epi wait_accf, -, total] summed over CTAs (lane 0 of warps 23, 12, 0)
+  if (G.dbg && lane == 0 && (warp == MMA_WARP || warp == NEPI || warp == 0)) {
+    const int role = warp == MMA_WARP ? 0 : (warp == NEPI ? 1 : 2);
+    atomicAdd(G.dbg + 3 * role + 0, (unsigned long long)tw[0]);
+    atomicAdd(G.dbg + 3 * role + 1, (unsigned long long)tw[1]);
+    atomicAdd(G.dbg + 3 * role + 2, (unsigned long long)(clock64() - tstart));
+  }
+  if (G.dbg && lane == 0 && (warp == NEPI || warp == NEPI + 1)) {  // producer detail: issuer warp, next warp
+    unsigned long long* q = G.dbg + 16 + 8 * (warp - NEPI);
+    for (int k = 0; k < 6; ++k) atomicAdd(q + k, (unsigned long long)tw[k]);
+    atomicAdd(q + 6, (unsigned long long)(clock64() - tstart));
+  }
+#endif
+  (void)tw;
+  (void)tstart;
   tc05::fence_before();
   __syncthreads();
   if (warp == MMA_WARP) {

@@ -1,0 +1,2 @@
+cd $GRAFT_REPO_ROOT
+timeout 120 python scripts/with_variant.py libnent_b200_timers.so scripts/m3_time.py 1 > gpurun_out/q_timers.log 2>&1

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 120 python scripts/m3_time.py 20 > gpurun_out/s_main.log 2>&1
+timeout 120 python scripts/with_variant.py libnent_b200_s2n9.so scripts/m3_time.py 20 > gpurun_out/s_s2n9.log 2>&1
+timeout 120 python scripts/with_variant.py libnent_b200_s3n6t.so scripts/m3_time.py 1 > gpurun_out/s_timers.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -m gpu -x -p no:cacheprovider -k "m3" > gpurun_out/s_tests.log 2>&1; echo "rc=$?" >> gpurun_out/s_tests.log

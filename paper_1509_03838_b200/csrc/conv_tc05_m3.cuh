@@ -23,15 +23,16 @@
 // its 16 outputs at once and recovers d_P, d_{P+1}, d_{P+2}; with failed =
 // None the redundant stream P follows and is checked against the recovery.
 //
-// CTA: 20 warps = 5 warpgroups, one persistent CTA per SM; a tile is 48
-// blocks of 128 outputs (MMA N = 48) of each stream.
-//   warps 0-11  epilogue (3 per TMEM lane quadrant, 16 accumulator columns
-//               each; 128 registers after setmaxnreg)
-//   warps 12-18 producers: TMA bulk copies of the raw int32 windows into a
-//               9-deep staging ring, split into byte planes (2 tile slots)
-//   warp 19     TMEM allocation; one elected lane issues every tcgen05.mma
-// TMEM: [0, 8*NG*NSTEPS) the Toeplitz tap digits (A operand), [192, 480) a
-// ring of 6 accumulator slots of 48 columns.
+// CTA: 16 warps = 4 warpgroups, one persistent CTA per SM; a tile is 64
+// blocks of 128 outputs (MMA N = 64) of each stream.
+//   warps 0-7   epilogue (2 per TMEM lane quadrant, 32 accumulator columns
+//               each; 184 registers after setmaxnreg)
+//   warps 8-14  producers: each warp TMA-copies its own 5 KB share of every
+//               raw int32 window into its own staging ring and splits it into
+//               byte planes (2 tile slots)
+//   warp 15     TMEM allocation; one elected lane issues every tcgen05.mma
+// TMEM: [0, 8*NG*NSTEPS) the Toeplitz tap digits (A operand), [192, 512) a
+// ring of 5 accumulator slots of 64 columns.
 #pragma once
 #include "conv_tc05.cuh"
 
@@ -50,45 +51,43 @@ using tcc::mb_expect_tx;
 using tcc::mb_init;
 using tcc::mb_wait;
 using tcc::mb_wait_sleep;
+using tcc::ld_cols;
 using tcc::sts32;
 
-constexpr int U = 48;                  // 128-position blocks per tile = MMA N
+constexpr int U = 64;                  // 128-position blocks per tile = MMA N
 constexpr int TILE = 128 * U;          // outputs per tile and stream
-constexpr int NEPI = 12;               // epilogue warps (3 per TMEM lane quadrant)
+constexpr int NEPI = 8;                // epilogue warps (2 per TMEM lane quadrant)
 constexpr int NPROD = 7;               // producer warps
-constexpr int MMA_WARP = NEPI + NPROD; // 19
+constexpr int MMA_WARP = NEPI + NPROD; // 15: the highest warp id has issue priority
 constexpr int NT = 32 * (NEPI + NPROD + 1);
-constexpr int EC = U / (NEPI / 4);     // 16 accumulator columns per epilogue thread
-constexpr int PT = 32 * NPROD;         // producer threads
-constexpr int HALFW = 4;               // int4 words per producer thread and half window
-constexpr int NWP = 2 * HALFW * PT;    // int4 words staged per raw stream and tile (1792)
-constexpr uint32_t HALFB = HALFW * PT * 16;  // bytes per staging unit (14,336)
+constexpr int EC = U / (NEPI / 4);     // 32 accumulator columns per epilogue thread
+// Each producer warp owns a contiguous 1/NPROD of every raw stream's window
+// (WW int4 per lane, 5 KB per warp) and stages it through its own TMA ring of
+// NSTAGE chunks: the warps never wait for each other.
+constexpr int WW = 10;                 // int4 words per lane and raw-stream window
+constexpr int NWP = WW * 32 * NPROD;   // int4 words staged per raw stream and tile (2240)
 #ifndef NENT_M3_NSTAGE
-#define NENT_M3_NSTAGE 4
+#define NENT_M3_NSTAGE 3
 #endif
 #ifndef NENT_M3_NSLOT
 #define NENT_M3_NSLOT 2
 #endif
 constexpr int NSLOT = NENT_M3_NSLOT;   // tile slots of byte planes: producers run up to NSLOT-1 tiles ahead
-// Each producer warp owns a contiguous 1/NPROD of every
-// raw stream's window (WW int4 per lane, 4 KB per warp) and stages it through
-// its own TMA ring of NSTAGE chunks: the warps never wait for each other.
 constexpr int NSTAGE = NENT_M3_NSTAGE;  // per-warp staging ring depth (NSTAGE-1 units in flight)
-constexpr int WW = 2 * HALFW;           // int4 words per lane and raw-stream window (8)
-constexpr uint32_t WCHUNK = WW * 32 * 16;  // bytes per warp and unit (4096)
-constexpr int PLANE = 7168;            // bytes per byte plane: >= 4 * NWP, 1024-aligned
+constexpr uint32_t WCHUNK = WW * 32 * 16;  // bytes per warp and unit (5120)
+constexpr int PLANE = 9216;            // bytes per byte plane: >= 4 * NWP, 1024-aligned
 constexpr int SLOTB = 6 * PLANE;       // one tile slot: 3 raw streams x {lo, hi}
 constexpr int TAPCOLS = 192;
 constexpr int RING0 = TAPCOLS;
-constexpr int SLOTS = (512 - RING0) / U;  // 6
-constexpr int LAUNCH_REGS = 96;        // 65536 / 640 rounded down to 8
-constexpr int EPI_REGS = 112, PROD_REGS = 72;
+constexpr int SLOTS = (512 - RING0) / U;  // 5
+constexpr int LAUNCH_REGS = 128;       // 65536 / 512
+constexpr int EPI_REGS = 184, PROD_REGS = 72;
 static_assert(NEPI * 32 * EPI_REGS + (NPROD + 1) * 32 * PROD_REGS <= NT * LAUNCH_REGS, "launch register pool");
 static_assert(NEPI % 4 == 0 && (NPROD + 1) % 4 == 0, "setmaxnreg acts on whole warpgroups");
 static_assert(4 * NWP >= TILE + 256, "a staged window covers the tile plus the K <= 257 halo");
 static_assert(4 * NWP <= PLANE, "a staged window fits its plane");
 constexpr uint32_t SSTR = WCHUNK + 128;  // staging slot stride: a chunk plus one int4 of lead-in
-constexpr size_t SMEM = NSLOT * (size_t)SLOTB + (size_t)NPROD * NSTAGE * SSTR;  // 204,288 B
+constexpr size_t SMEM = NSLOT * (size_t)SLOTB + (size_t)NPROD * NSTAGE * SSTR;  // 220,800 B
 static_assert(SMEM + 1024 <= 227 * 1024, "shared memory");
 
 struct Geom {
@@ -120,6 +119,22 @@ __device__ __forceinline__ void split2(int4 v, uint32_t& lo, uint32_t& hi) {
   const uint32_t t01 = __byte_perm(u0, u1, 0x5140), t23 = __byte_perm(u2, u3, 0x5140);
   lo = __byte_perm(t01, t23, 0x5410);
   hi = __byte_perm(t01, t23, 0x7632);
+}
+
+// this thread's EC accumulator columns of one slot, as x16 loads (16-register
+// blocks keep the register allocation flexible; x32 needs 32 aligned ones)
+template <int N>
+__device__ __forceinline__ void ld_slot(uint32_t taddr, uint32_t (&r)[N]) {
+#pragma unroll
+  for (int k = 0; k < N / 16; ++k) tc05::ld_x16(taddr + 16u * k, *reinterpret_cast<uint32_t(*)[16]>(r + 16 * k));
+}
+
+// mbarrier wait that suspends the warp in hardware until the phase completes
+// (or a 20 us hint expires) instead of polling with try_wait + nanosleep
+__device__ __forceinline__ void mb_wait_suspend(uint32_t mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n M3_WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra M3_WAITS_%=;\n}" ::"r"(mb), "r"(parity), "r"(20000) : "memory");
 }
 
 // Register pins: an empty volatile asm that reads and rewrites x, ordered
@@ -158,6 +173,19 @@ __device__ __forceinline__ void fold_ab(uint64_t (&C)[N], uint32_t (&lowA)[N], c
     sub_shifted<8 * CL>(C[i], rB[i]);
     if (CL < 4) lowA[i] += rA[i] << (8 * CL);
   }
+}
+template <int CL, int N>
+__device__ __forceinline__ void fold_a(uint64_t (&C)[N], uint32_t (&lowA)[N], const uint32_t (&rA)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    add_shifted<8 * CL + 16>(C[i], rA[i]);
+    if (CL < 4) lowA[i] += rA[i] << (8 * CL);
+  }
+}
+template <int CL, int N>
+__device__ __forceinline__ void fold_b(uint64_t (&C)[N], const uint32_t (&rB)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) sub_shifted<8 * CL>(C[i], rB[i]);
 }
 template <int CL, int N>
 __device__ __forceinline__ void fold_p(uint64_t (&acc)[N], const uint32_t (&r)[N]) {
@@ -266,16 +294,19 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     // trip: both loads, one wait), which are then handed back to the MMA warp
     auto drain2 = [&](uint32_t (&ra)[EC], uint32_t (&rb)[EC], bool two) {
       const int r0 = kslot % SLOTS, r1 = (kslot + 1) % SLOTS;
-#ifdef NENT_M3_EPI_SPIN
+#if defined(NENT_M3_EPI_SPIN)
       TM(0, mb_wait(accf_b(r0), (uint32_t)((kslot / SLOTS) & 1)));
       if (two) TM(0, mb_wait(accf_b(r1), (uint32_t)(((kslot + 1) / SLOTS) & 1)));
+#elif defined(NENT_M3_EPI_SUSPEND)
+      TM(0, mb_wait_suspend(accf_b(r0), (uint32_t)((kslot / SLOTS) & 1)));
+      if (two) TM(0, mb_wait_suspend(accf_b(r1), (uint32_t)(((kslot + 1) / SLOTS) & 1)));
 #else
       TM(0, mb_wait_sleep(accf_b(r0), (uint32_t)((kslot / SLOTS) & 1)));
       if (two) TM(0, mb_wait_sleep(accf_b(r1), (uint32_t)(((kslot + 1) / SLOTS) & 1)));
 #endif
       tc05::fence_after();
-      tc05::ld_x16(tbase + lrow + (uint32_t)(RING0 + r0 * U + EC * part), ra);
-      if (two) tc05::ld_x16(tbase + lrow + (uint32_t)(RING0 + r1 * U + EC * part), rb);
+      ld_slot(tbase + lrow + (uint32_t)(RING0 + r0 * U + EC * part), ra);
+      if (two) ld_slot(tbase + lrow + (uint32_t)(RING0 + r1 * U + EC * part), rb);
       tc05::wait_ld();
       tc05::fence_before();
       __syncwarp();
@@ -315,10 +346,14 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       // the next classes' TMEM loads and spill the extra live registers) whose
       // body switches to a fold with compile-time class weights: every term is
       // one IMAD.WIDE (or one IMAD on the high word for weights >= 2^32).
+#ifdef NENT_M3_UNROLL_CLASSES
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
       for (int c = 0; c < NCLS; ++c) {
         uint32_t rA[EC], rB[EC];
-        drain2(rA, rB, true);
+        drain2(rA, rB, true);  // class c of delta_A and of delta_B: consecutive ring slots
         switch (c) {
           case 0: fold_ab<0>(C, lowA, rA, rB); break;
           case 1: fold_ab<1>(C, lowA, rA, rB); break;
@@ -335,6 +370,13 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         const int32_t d1 = (int32_t)(lowA[i] - ((uint32_t)d0 << 16));
         const int64_t o = o0 + 128 * i;
         if (interior || (o >= 0 && o < A.n_out)) {
+#ifdef NENT_M3_CHECK
+          if (o < 0 || o >= A.n_out) {
+            printf("M3CHECK store cta %d tile %lld o %lld n_out %lld\n", blockIdx.x, (long long)tile, (long long)o,
+                   (long long)A.n_out);
+            __trap();
+          }
+#endif
           yP[o] = d0;
           yA[o] = d1;
           yB[o] = (int32_t)(0u - (uint32_t)vv);
@@ -343,15 +385,17 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         // (d_{P+2} << 16) + d_P: start its fold at minus that
         accP[i] = corr - ((uint64_t)(int64_t)d0 - ((uint64_t)(int64_t)vv << 16));
       }
+#ifndef NENT_M3_NOVERIFY_DBG
       if (verify) {  // the redundant stream P, two classes per drain
 #pragma unroll 1
-        for (int c = 0; c < NCLS; c += 2) {
+        for (int c = 0; c < NCLS; ++c) {
           uint32_t r0[EC], r1[EC];
-          const bool two = c + 1 < NCLS;
-          drain2(r0, r1, two);
+          drain2(r0, r1, false);
           switch (c) {
-            case 0: fold_p<0>(accP, r0); fold_p<1>(accP, r1); break;
-            case 2: fold_p<2>(accP, r0); if (two) fold_p<3>(accP, r1); break;
+            case 0: fold_p<0>(accP, r0); break;
+            case 1: fold_p<1>(accP, r0); break;
+            case 2: fold_p<2>(accP, r0); break;
+            case 3: fold_p<3>(accP, r0); break;
             default: fold_p<4>(accP, r0); break;
           }
         }
@@ -361,6 +405,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
           bad += (interior || (o >= 0 && o < A.n_out)) && accP[i] != 0;
         }
       }
+#endif
     }
     if (A.mismatch) {
 #pragma unroll
@@ -457,6 +502,19 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
             const int d = dph_of(is);
             const char* src = reinterpret_cast<const char*>(row_of(is) + iP0 - d) + (size_t)wbase * 16;
             const uint32_t bytes = WCHUNK + (d ? 16u : 0u);
+#ifdef NENT_M3_CHECK
+            {
+              const int64_t first = iP0 - d + wbase * 4, last = first + bytes / 4;
+              const uint32_t dst = ring + (uint32_t)b * SSTR;
+              if (first < 0 || last > A.n_in || (reinterpret_cast<uintptr_t>(src) & 15) || (dst & 15) ||
+                  dst + bytes > planes_s + (uint32_t)SMEM) {
+                printf("M3CHECK tma cta %d warp %d is %d P0 %lld d %d first %lld last %lld n_in %lld dst %u end %u\n",
+                       blockIdx.x, pw, is, (long long)iP0, d, (long long)first, (long long)last, (long long)A.n_in,
+                       dst, planes_s + (uint32_t)SMEM);
+                __trap();
+              }
+            }
+#endif
             mb_expect_tx(stg_b(pw, b), bytes);
             bulk_g2s(ring + (uint32_t)b * SSTR, src, bytes, stg_b(pw, b));
             ++issued;
@@ -485,22 +543,24 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
           const int d = dph_of(s);
           TM(4, {
 #pragma unroll
-          for (int i0 = 0; i0 < WW; i0 += 4) {
-            int4 v[4];
+          for (int i0 = 0; i0 < WW; i0 += 5) {  // two batches of 5 words (WW = 10)
+            constexpr int B = 5;
+            static_assert(WW % B == 0, "batches cover the lane's words");
+            int4 v[B];
             if (d == 0) {
               const int4* sb = reinterpret_cast<const int4*>(__cvta_shared_to_generic(sbuf));
 #pragma unroll
-              for (int i = 0; i < 4; ++i) v[i] = sb[(i0 + i) * 32 + lane];
+              for (int i = 0; i < B; ++i) v[i] = sb[(i0 + i) * 32 + lane];
             } else {  // this row's window starts d words into the staged copy
               const uint32_t* sw = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
+              for (int i = 0; i < B; ++i) {
                 const uint32_t* q = sw + 4 * ((i0 + i) * 32 + lane);
                 v[i] = make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]);
               }
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < B; ++i) {
               uint32_t lo, hi;
               split2(v[i], lo, hi);
               const uint32_t off = soff(i0 + i);

@@ -22,7 +22,7 @@ OBJ = PKG / "_obj"
 LIB = PKG / "libnent_b200.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(INCLUDE)]
+NVCC_FLAGS = ARCH + ["--compress-mode=size", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(INCLUDE)]
 
 
 def _nvcc() -> str:

@@ -74,14 +74,13 @@ int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
     unsigned long long h[64];
     cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    fprintf(stderr, "m3 timers (kcycles/CTA): mma wait_full %.1f wait_acce %.1f total %.1f | epi wait_accf %.1f total %.1f"
-            " | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid, h[6] / 1e3 / grid,
-            h[8] / 1e3 / grid, (double)G.ntiles / grid);
+    fprintf(stderr, "m3 timers (kcycles/CTA): mma wait_full %.1f wait_acce %.1f total %.1f | loader wait_free %.1f total %.1f"
+            " | epi wait_accf %.1f total %.1f | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid,
+            h[3] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[8] / 1e3 / grid, (double)G.ntiles / grid);
     for (int w = 0; w < 2; ++w) {
       const unsigned long long* q = h + 16 + 8 * w;
-      fprintf(stderr, "  producer warp %d: wait_empty %.1f wait_tma %.1f issue+sync %.1f load %.1f convert+sts %.1f "
-              "tail %.1f total %.1f\n", w, q[0] / 1e3 / grid, q[1] / 1e3 / grid, q[2] / 1e3 / grid, q[3] / 1e3 / grid,
-              q[4] / 1e3 / grid, q[5] / 1e3 / grid, q[6] / 1e3 / grid);
+      fprintf(stderr, "  converter warp %d: wait_empty %.1f wait_stage %.1f convert+sts %.1f total %.1f\n", w,
+              q[0] / 1e3 / grid, q[1] / 1e3 / grid, q[4] / 1e3 / grid, q[6] / 1e3 / grid);
     }
   }
 #endif

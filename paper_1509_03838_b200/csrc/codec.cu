@@ -220,6 +220,44 @@ entangle_vec_kernel(const Rows src, MutRows eps, int m, int64_t n, int64_t head,
   }
 }
 
+// All MT rows of a position vector in one thread: every source word is read
+// from HBM exactly once (the row-per-block kernel above reads each row twice,
+// as c_i and as c_{i-1}, and the second read misses L2 on streams beyond its
+// 126 MB), so the pass moves the algorithmic m*n words in and m*n words out.
+template <int MT, typename TI, typename TO>
+__global__ void __launch_bounds__(EW_THREADS)
+entangle_rows_kernel(const Rows src, MutRows eps, int64_t n, int64_t head, int64_t nq, int l, int64_t hi,
+                     int check, unsigned long long* bad) {
+  auto one = [&](int i, int64_t j, int64_t a, int64_t b) {
+    if (check && wabs(b) > hi) atomicMin(bad, (unsigned long long)((int64_t)i * n + j));
+    return wadd(wshl(a, l), b);
+  };
+  const int64_t stride = (int64_t)gridDim.x * EW_THREADS;
+  for (int64_t q = (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; q < nq; q += stride) {
+    int64_t c[MT][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) load4(reinterpret_cast<const TI*>(src.p[i]), head + 4 * q, c[i]);
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      int64_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = one(i, head + 4 * q + k, c[(i + MT - 1) % MT][k], c[i][k]);
+      store4(reinterpret_cast<TO*>(eps.p[i]), head + 4 * q, o);
+    }
+  }
+  if (blockIdx.x == 0) {  // the unaligned head [0, head) and the ragged tail [head + 4 nq, n)
+    const int64_t tail0 = head + 4 * nq, ns = head + (n - tail0);
+    for (int64_t k = threadIdx.x; k < ns * MT; k += EW_THREADS) {
+      const int i = (int)(k / ns);
+      const int64_t kk = k - (int64_t)i * ns;
+      const int64_t j = kk < head ? kk : tail0 + (kk - head);
+      reinterpret_cast<TO*>(eps.p[i])[j] =
+          (TO)(uint64_t)one(i, j, (int64_t)__ldg(reinterpret_cast<const TI*>(src.p[(i + MT - 1) % MT]) + j),
+                            (int64_t)__ldg(reinterpret_cast<const TI*>(src.p[i]) + j));
+    }
+  }
+}
+
 template <int MT, typename TI, typename TO>
 __global__ void __launch_bounds__(EW_THREADS)
 extract_vec_kernel(const Rows delta, MutRows out, int64_t n, int64_t head, int64_t nq, int l, int r, int wide,
@@ -456,6 +494,23 @@ int nent_entangle(const void* const* src, int src_bits, void* const* eps, int ep
   Rows R = to_rows(src, m);
   MutRows W = to_mrows(eps, m);
   const int64_t head = n >= 64 ? common_head(src, m, src_bits, eps, m, eps_bits, -1) : -1;
+  if (head >= 0 && (m == 3 || m == 4 || m == 8)) {  // all rows per thread: each word read once
+    const int64_t nq = (n - head) / 4;
+    const int grid = grid_for(nq, EW_THREADS, 1, 148 * 8);
+#define NENT_ROWS_CASE(MT)                                                                     \
+  DISPATCH_IO(src_bits, eps_bits,                                                              \
+              (entangle_rows_kernel<MT, TI, TO><<<grid, EW_THREADS, 0, s>>>(                   \
+                  R, W, n, head, nq, l, check_hi, check, (unsigned long long*)bad_index_dev)))
+    if (m == 3) {
+      NENT_ROWS_CASE(3);
+    } else if (m == 4) {
+      NENT_ROWS_CASE(4);
+    } else {
+      NENT_ROWS_CASE(8);
+    }
+#undef NENT_ROWS_CASE
+    return check_launch("entangle");
+  }
   if (head >= 0) {  // 16-byte vectors
     const int64_t nq = (n - head) / 4;
     dim3 grid(grid_for(nq, EW_THREADS, 2, 148 * 16 / (m > 4 ? 4 : 1)), m);

@@ -26,7 +26,10 @@ bool tc05_m3_envelope(const ConvArgs& A, int np, int ng) {
   for (int i = 0; i < 3; ++i)
     if (!A.a.p[i] || !A.b.p[i] || !A.y.p[i]) return false;  // raw streams, entangled on load
   if (A.perm || A.add || A.scale != 1 || A.wide) return false;
-  if (A.period < A.n_in + A.K - 1) return false;  // zero-padded (full) convolution only
+  // the kernel zero-extends the rows instead of wrapping: a zero-padded (full)
+  // convolution, or an output window no tap of which wraps around the period
+  // (the chunked host pipeline's and the halo-split shards' windows)
+  if (A.period < A.n_in + A.K - 1 && !(A.y_begin >= A.K - 1 && A.y_begin + A.n_out <= A.period)) return false;
   if (A.K < 1 || A.K > 257) return false;
   for (int i = 0; i < 3; ++i)  // int32 rows: 4-byte aligned
     if (reinterpret_cast<uintptr_t>(A.b.p[i]) & 3) return false;
@@ -77,6 +80,11 @@ int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
     fprintf(stderr, "m3 timers (kcycles/CTA): mma wait_full %.1f wait_acce %.1f total %.1f | loader wait_free %.1f total %.1f"
             " | epi wait_accf %.1f total %.1f | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid,
             h[3] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[8] / 1e3 / grid, (double)G.ntiles / grid);
+    fprintf(stderr, "  mma wait per slot position (A0 B0 A1 B1 .. A4 B4 P0..P4):");
+    for (int k = 0; k < 15; ++k) fprintf(stderr, " %.1f", h[32 + k] / 1e3 / grid);
+    fprintf(stderr, "\n  epilogue wait per step (AB0..AB4, P01, P23, P4):");
+    for (int k = 0; k < 8; ++k) fprintf(stderr, " %.1f", h[48 + k] / 1e3 / grid);
+    fprintf(stderr, "\n");
     for (int w = 0; w < 2; ++w) {
       const unsigned long long* q = h + 16 + 8 * w;
       fprintf(stderr, "  converter warp %d: wait_empty %.1f wait_stage %.1f convert+sts %.1f total %.1f\n", w,

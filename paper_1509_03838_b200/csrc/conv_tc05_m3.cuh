@@ -216,11 +216,32 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
   tc05::fence_after();
   if (tmem_slot != 0 || (planes_s & 1023u)) __trap();
   constexpr uint32_t tbase = 0;
+  const int my_tiles = G.ntiles > blockIdx.x ? (int)((G.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  // the first input sample of this CTA's t-th tile's windows (row 0's phase)
+  const int64_t P0_first = A.y_begin - G.shift + (int64_t)blockIdx.x * TILE - (G.KT - 128);
+  const int64_t P0_step = (int64_t)gridDim.x * TILE;
+  // a tile is staged by TMA iff its whole window lies inside the streams
+  auto staged = [&](int64_t P0) { return P0 >= 4 && P0 + 4 * (int64_t)NWP + 4 <= A.n_in; };
+  // one raw window: row s from dph[s] words earlier, so every source is 16-byte aligned
+  auto issue_window = [&](int s, int64_t P0, int b) {
+    const int d = G.dph[s];
+    const char* src = reinterpret_cast<const char*>(reinterpret_cast<const int32_t*>(A.b.p[s]) + P0 - d);
+    const uint32_t bytes = WINB + (d ? 16u : 0u);
+    mb_expect_tx(sfull_b(b), bytes);
+    bulk_g2s(stage_s + (uint32_t)b * SSTR, src, bytes, sfull_b(b));
+  };
+  // the first tile's windows are in flight while the tap table is built
+  constexpr int PRE = NSTAGE < 3 ? NSTAGE : 3;
+  const bool pre_issue = my_tiles > 0 && staged(P0_first);
+  if (pre_issue && warp == LOAD_WARP && lane == 0) {
+#pragma unroll
+    for (int s = 0; s < PRE; ++s) issue_window(s, P0_first, s);
+  }
   {
-    // the reversed taps' digits, staged once in the (still free) staging ring:
+    // the reversed taps' digits, staged once in the (still free) last plane slot:
     // rev[j][i] = digit_j(g[KT-1-i]), A_j[v][k] = rev[j][k - v + 127]
     const int RL = G.KT + 128;
-    unsigned char* rev = smem_raw + NSLOT * SLOTB;
+    unsigned char* rev = smem_raw + (NSLOT - 1) * SLOTB;
     const uint64_t gbias = bias_of(NG);
     for (int i = tid; i < RL; i += NT) {
       const int idx = G.KT - 1 - i;
@@ -242,19 +263,18 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     }
     tc05::wait_st();
     tc05::fence_before();
-    __syncthreads();  // also: the taps' staging bytes are dead before the loader's first copy lands
+    __syncthreads();  // also: the taps' staging bytes are dead before a converter writes that plane slot
     tc05::fence_after();
   }
   const bool verify = A.r < 0;
   const int P = verify ? 0 : A.r;  // pivot: the stream never read (or checked last)
   const int sA = P + 1 >= 3 ? P - 2 : P + 1, sB = P + 2 >= 3 ? P - 1 : P + 2;
-  const int my_tiles = G.ntiles > blockIdx.x ? (int)((G.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  // the first input sample of this CTA's t-th tile's windows (row 0's phase)
-  const int64_t P0_first = A.y_begin - G.shift + (int64_t)blockIdx.x * TILE - (G.KT - 128);
-  const int64_t P0_step = (int64_t)gridDim.x * TILE;
-  // a tile is staged by TMA iff its whole window lies inside the streams
-  auto staged = [&](int64_t P0) { return P0 >= 4 && P0 + 4 * (int64_t)NWP + 4 <= A.n_in; };
   long long tw[6] = {0, 0, 0, 0, 0, 0};
+#ifdef NENT_TC05_TIMERS
+  long long twk[16] = {0};
+  int estep = 0;
+  (void)estep;
+#endif
   const long long tstart = clock64();
 
   if (warp >= EPI0 && warp < EPI0 + NEPI) {
@@ -273,8 +293,15 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     static_assert(EH == 16, "half steps are x16 TMEM loads");
     auto class_step = [&](bool two, auto&& f) {
       const int r0 = kslot % SLOTS, r1 = (kslot + 1) % SLOTS;
+#ifdef NENT_TC05_TIMERS
+      const long long tq_ = clock64();
+#endif
       TM(0, mb_wait_sleep(accf_b(r0), (uint32_t)((kslot / SLOTS) & 1)));
       if (two) TM(0, mb_wait_sleep(accf_b(r1), (uint32_t)(((kslot + 1) / SLOTS) & 1)));
+#ifdef NENT_TC05_TIMERS
+      twk[estep] += clock64() - tq_;
+      estep = estep == 7 ? 0 : estep + 1;
+#endif
       tc05::fence_after();
       const uint32_t t0 = tbase + lrow + (uint32_t)(RING0 + r0 * U + EC * part);
       const uint32_t t1 = tbase + lrow + (uint32_t)(RING0 + r1 * U + EC * part);
@@ -448,14 +475,26 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         TM(0, mb_wait(full_b(ts), (uint32_t)((t / NSLOT) & 1)));
         tc05::fence_after();
         if (elect_one()) {
+#ifdef NENT_TC05_TIMERS
+          int kpos = 0;
+#endif
           const uint32_t slot_s = planes_s + (uint32_t)(ts * SLOTB);
           // chains of stream i's class c into the next ring slot
           auto issue_class = [&](int i, int c) {
             const int rs = kslot % SLOTS, use = kslot / SLOTS;
             if (use >= 1) {
+#ifdef NENT_TC05_TIMERS
+              const long long tq_ = clock64();
+#endif
               TM(1, mb_wait(acce_b(rs), (uint32_t)((use - 1) & 1)));
+#ifdef NENT_TC05_TIMERS
+              twk[kpos] += clock64() - tq_;
+#endif
               tc05::fence_after();
             }
+#ifdef NENT_TC05_TIMERS
+            ++kpos;
+#endif
             const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
             const int im1 = i == 0 ? 2 : i - 1;
             bool first = true;
@@ -494,9 +533,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         mb_wait(empty_b(t % NSLOT), (uint32_t)((t / NSLOT) & 1));
     } else if (warp == LOAD_WARP) {
       // ---------------- loader ----------------
-      // One thread: every staged tile's three raw windows, one bulk copy each
-      // (row s from dph[s] words earlier, so every source is 16-byte aligned),
-      // as soon as a staging buffer is free.
+      // One thread: every staged tile's three raw windows, one bulk copy each,
+      // as soon as a staging buffer is free (the first PRE went out above).
       if (lane == 0) {
         int64_t P0 = P0_first;
         int issued = 0;
@@ -505,12 +543,10 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
 #pragma unroll
           for (int s = 0; s < 3; ++s) {
             const int b = issued % NSTAGE;
-            if (issued >= NSTAGE) TM(0, mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1)));
-            const int d = dph_of(s);
-            const char* src = reinterpret_cast<const char*>(row_of(s) + P0 - d);
-            const uint32_t bytes = WINB + (d ? 16u : 0u);
-            mb_expect_tx(sfull_b(b), bytes);
-            bulk_g2s(stage_s + (uint32_t)b * SSTR, src, bytes, sfull_b(b));
+            if (!(pre_issue && issued < PRE)) {
+              if (issued >= NSTAGE) TM(0, mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1)));
+              issue_window(s, P0, b);
+            }
             ++issued;
           }
         }
@@ -608,6 +644,9 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     atomicAdd(G.dbg + 3 * role + 0, (unsigned long long)tw[0]);
     atomicAdd(G.dbg + 3 * role + 1, (unsigned long long)tw[1]);
     atomicAdd(G.dbg + 3 * role + 2, (unsigned long long)(clock64() - tstart));
+  }
+  if (G.dbg && lane == 0 && (warp == MMA_WARP || warp == EPI0)) {  // per-position waits: [32..47] MMA, [48..63] epilogue
+    for (int k = 0; k < 16; ++k) atomicAdd(G.dbg + (warp == MMA_WARP ? 32 : 48) + k, (unsigned long long)twk[k]);
   }
   if (G.dbg && lane == 0 && (warp == CONV0 || warp == CONV0 + 1)) {
     unsigned long long* q = G.dbg + 16 + 8 * (warp - CONV0);

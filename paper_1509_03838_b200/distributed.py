@@ -27,6 +27,12 @@ the plumbing:
   fused entangle -> conv -> extract kernel on [halo | slice].  Entangle and
   extract are position-local, so nothing else crosses ranks.
 
+* ``BatchSplit`` -- cfg4's batch of independent vectors (inner / outer
+  products against a shared vector, ops.py:205-227) cut into contiguous
+  vector ranges, one per rank: every vector's entangle -> product -> extract
+  is local, so the data path has no exchange at all (weak scaling); only the
+  optional gather of the recovered dots crosses ranks.
+
 Compute goes through a ``compute`` object (default ``DeviceCompute``: the
 sm_100a kernels); the CPU tests inject a CPU stand-in to exercise the
 exchange logic under gloo, and the GPU tests run ``DeviceCompute`` with
@@ -96,6 +102,17 @@ class DeviceCompute:
         g_dev = D.taps_tensor(np.asarray(g, dtype=np.int64), flavor)
         return D.fused_conv(x, g_dev, len(g), params.l, flavor, failed, params.w > 32, period,
                             n_in=n_in, y_begin=y_begin, n_out=n_out)
+
+
+    def fused_inner(self, c, params: CodecParams, g, failed=None):
+        from .fused import entangled_inner
+
+        return entangled_inner(params, c, g, failed=failed)
+
+    def fused_outer(self, c, params: CodecParams, g, failed=None, out=None, sums=None):
+        from .fused import entangled_outer
+
+        return entangled_outer(params, c, g, failed=failed, out=out, sums=sums)
 
 
 def _host_exchange(group) -> bool:
@@ -382,3 +399,50 @@ class HaloSplit:
         if self.rank != dst:
             return None
         return torch.cat([p[:, : int(s.item())] for p, s in zip(parts, all_sizes)], dim=1).to(d_local.device)
+
+
+@dataclass
+class BatchSplit:
+    """cfg4: ``batch`` independent vectors per stream, rank p
+    owns vectors shard_bounds(batch, world, p) of every stream.  Reference:
+    INNER_PRODUCT / ROW_GEMM over a batch (ops.py:205-227); each vector is its
+    own entangle -> op -> extract, so ranks never exchange data."""
+
+    params: CodecParams
+    group: object = None
+    compute: object = None
+
+    def __post_init__(self):
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        if self.compute is None:
+            self.compute = DeviceCompute()
+
+    def bounds(self, batch: int) -> tuple[int, int]:
+        return shard_bounds(batch, self.world, self.rank)
+
+    def inner(self, c_local: torch.Tensor, g, failed: int | None = None):
+        """Recovered dots (m, local batch) of this rank's vectors c_local
+        (m, local batch, n) against g; .mismatches is the redundant-stream check."""
+        if c_local.dim() != 3 or c_local.shape[0] != self.params.m:
+            raise ParameterError("BatchSplit.inner needs c of shape (m, local batch, n)")
+        return self.compute.fused_inner(c_local, self.params, g, failed=failed)
+
+    def outer(self, c_local: torch.Tensor, g, failed: int | None = None, out=None, sums=None):
+        """Outer products of this rank's vectors with g: written to ``out``
+        (m, local batch, n, p) and/or summed per (stream, vector) into ``sums``."""
+        return self.compute.fused_outer(c_local, self.params, g, failed=failed, out=out, sums=sums)
+
+    def gather(self, d_local: torch.Tensor, batch: int, dst: int = 0):
+        """All ranks' (m, local batch) results concatenated along the batch on ``dst``."""
+        m = d_local.shape[0]
+        width = -(-batch // self.world)
+        buf = d_local.new_zeros((m, width))
+        buf[:, : d_local.shape[1]] = d_local
+        buf = _to_x(buf, self.group)
+        parts = [torch.empty_like(buf) for _ in range(self.world)] if self.rank == dst else None
+        dist.gather(buf, parts, group=self.group, group_dst=dst)
+        if self.rank != dst:
+            return None
+        spans = [shard_bounds(batch, self.world, r) for r in range(self.world)]
+        return torch.cat([p[:, : e - b] for p, (b, e) in zip(parts, spans)], dim=1).to(d_local.device)

@@ -35,7 +35,7 @@ class ChunkedEntangledConv:
     -- per-row copies cost ~5% at 2^20-sample chunks and ~20% at 2^18.  Host
     transfers start on a 256-byte boundary (row 0's; other rows follow the
     caller's pitch): concurrent H2D + D2H loses ~20% when the host side is
-    misaligned (scripts/pcie_align_probe.py), so each input copy starts at the
+    misaligned (profiles/r01_e2e_pipeline.md), so each input copy starts at the
     aligned word at or below its window (the kernel reads its rows from
     ``PRE`` words in), and each chunk computes ``LEAD`` extra outputs before
     its window so its output copy can start at the aligned word at or below
@@ -47,7 +47,7 @@ class ChunkedEntangledConv:
     lockstep -- H2D(j+1) and D2H(j) share the link and finish together -- and
     every chunk's kernel then sits exposed on the D2H stream: an idle output
     direction does not make the input direction much faster, so the input
-    side never builds the lead that would hide it (scripts/e2e_isolate.py)."""
+    side never builds the lead that would hide it (profiles/r01_e2e_pipeline.md)."""
 
     def __init__(self, params: CodecParams, n: int, g, flavor: int, chunk: int = 1 << 20,
                  in_dtype=torch.int32, out_dtype=torch.int32, nbuf: int = 4,

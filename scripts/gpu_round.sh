@@ -1,5 +1,22 @@
-# bench (default args, as the driver runs it), reference arm, then the ncu passes
+# Evidence run of the committed build: smoke, GPU tests, bench (driver
+# protocol), reference arm, then the ncu passes (each after its own command
+# exited 0 without ncu).  Usage: gpurun -- 'bash scripts/gpu_round.sh TAG'
+TAG=${1:-r02}
 cd $GRAFT_REPO_ROOT
-timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "rc=$?" >> gpurun_out/bench_full.log
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref.log
-bash scripts/profile.sh
+timeout 300 python __graft_entry__.py --smoke > gpurun_out/${TAG}_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_smoke.log
+timeout 1800 python -m pytest tests -q -m gpu -x -p no:cacheprovider > gpurun_out/${TAG}_tests.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_tests.log
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv -lms 200 > gpurun_out/${TAG}_clocks.csv &
+SMI=$!
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_bench.log
+kill $SMI
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_ref.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_ref.log
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
+$CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+    --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
+echo "launches rc=$?" >> gpurun_out/${TAG}_plain.log
+CMD2="python scripts/m3_time.py 2"
+$CMD2 > gpurun_out/${TAG}_plain2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on --warp-sampling-interval 0 -k regex:conv_tc05_m3 -s 2 -c 1 \
+    -o gpurun_out/${TAG}_prof_m3 $CMD2 > gpurun_out/${TAG}_ncu_full.log 2>&1
+echo "full rc=$?" >> gpurun_out/${TAG}_plain2.log

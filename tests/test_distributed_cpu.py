@@ -58,6 +58,23 @@ class OracleCompute:
         return torch.from_numpy(O.disentangle(delta, params.m, params.l, params.w, failed))
 
 
+    def fused_inner(self, c, params, g, failed=None):
+        O = self.O
+        cn = c.numpy()
+        m, B, n = cn.shape
+        eps = O.entangle(cn.reshape(m, B * n), params.l).reshape(m, B, n)
+        delta = (eps * np.asarray(g)[None, None, :]).sum(axis=2)
+        if failed is not None:
+            delta[failed] = O.poison_pattern(params.w, B)
+
+        class R:
+            outputs = None
+            mismatches = 0
+        r = R()
+        r.outputs = torch.from_numpy(O.disentangle(delta, params.m, params.l, params.w, failed))
+        return r
+
+
 def _init(rank, world, port):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -155,6 +172,32 @@ def _halo_worker(rank, world, port, q):
         raise
 
 
+def _batch_worker(rank, world, port, q):
+    """cfg4's batch split: every rank's vectors are independent, no exchange."""
+    try:
+        _init(rank, world, port)
+        from paper_1509_03838_b200 import workloads
+        from paper_1509_03838_b200.distributed import BatchSplit
+        wl = workloads.make(4, batch=37, n=129)
+        drv = BatchSplit(wl.params, compute=OracleCompute())
+        b, e = drv.bounds(wl.c.shape[1])
+        ok = True
+        want = (wl.c * wl.g[None, None, :]).sum(axis=2)
+        for failed in (None, 0, 1, 2):
+            res = drv.inner(torch.from_numpy(wl.c[:, b:e].copy()), wl.g, failed=failed)
+            d = res.outputs if isinstance(res.outputs, torch.Tensor) else torch.from_numpy(res.outputs.data)
+            full = drv.gather(d, wl.c.shape[1])
+            if rank == 0:
+                ok = ok and np.array_equal(full.numpy(), want)
+        if rank == 0:
+            q.put(ok)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        q.put(repr(exc))
+        raise
+
+
 def _spawn(fn, world, *args):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -186,6 +229,11 @@ def test_sub_group_peers_are_group_local():
 @pytest.mark.parametrize("world", [2, 3])
 def test_halo_split(world):
     assert _spawn(_halo_worker, world) is True
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_split_cfg4(world):
+    assert _spawn(_batch_worker, world) is True
 
 
 def test_shard_bounds_cover():

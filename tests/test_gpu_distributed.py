@@ -110,6 +110,45 @@ def _halo_worker(rank, world, port, q):
         raise
 
 
+def _batch_worker(rank, world, port, q):
+    """cfg4's batch split with the device kernels: inner products of every
+    rank's vector range for every failure, gathered and checked; outer-product
+    sums of the local range against the closed form."""
+    try:
+        _init(rank, world, port)
+        from paper_1509_03838_b200 import workloads
+        from paper_1509_03838_b200.distributed import BatchSplit
+
+        wl = workloads.make(4, batch=203, n=4096)
+        drv = BatchSplit(wl.params)
+        dev = torch.device("cuda", 0)
+        B = wl.c.shape[1]
+        b, e = drv.bounds(B)
+        c_local = torch.from_numpy(wl.c[:, b:e].copy()).to(dev).to(torch.int32)
+        want = (wl.c * wl.g[None, None, :]).sum(axis=2)
+        ok = {}
+        for failed in (None, 0, 1, 2):
+            res = drv.inner(c_local, wl.g, failed=failed)
+            full = drv.gather(res.outputs.data, B)
+            if rank == 0:
+                ok[("inner", failed)] = bool(np.array_equal(full.to(torch.int64).cpu().numpy(), want))
+            sums = torch.zeros((3, e - b), dtype=torch.int64, device=dev)
+            drv.outer(c_local, wl.g, failed=failed, sums=sums)
+            closed = wl.c[:, b:e].sum(axis=2) * int(wl.g.sum())  # sum_{u,v} c[u] g[v]
+            good = bool(np.array_equal(sums.cpu().numpy(), closed))
+            goods = [None] * world
+            dist.all_gather_object(goods, good)
+            if rank == 0:
+                ok[("outer_sums", failed)] = all(goods)
+        if rank == 0:
+            q.put(ok)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        q.put(repr(exc))
+        raise
+
+
 def _spawn(fn, world, *args, timeout=600):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -157,3 +196,8 @@ def test_stream_per_gpu_cfg5_full_size_digest():
 @pytest.mark.parametrize("world", [2, 3])
 def test_halo_split_device(world):
     _all_true(_spawn(_halo_worker, world))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_batch_split_device(world):
+    _all_true(_spawn(_batch_worker, world))

@@ -24,8 +24,12 @@ def pinned_view(rows, cols, off, dtype=torch.int32):
 @pytest.mark.parametrize("n,K,chunk,off", [(50000, 256, 1 << 13, 0), (70001, 255, 1 << 14, 1),
                                            (4096, 1, 1024, 3), (300, 64, 1 << 15, 2),
                                            (123457, 97, 1 << 15, 5)])
-def test_chunked_pipeline_matches_oracle(oracle, n, K, chunk, off):
-    p = nent.derive_params(3, 64)
+@pytest.mark.parametrize("w", [48, 64])
+def test_chunked_pipeline_matches_oracle(oracle, n, K, chunk, off, w):
+    # w = 48: the (3,48,16,16) geometry, whose chunks run on the fused m = 3
+    # tcgen05 kernel (non-wrapping windows); w = 64: the generic tcgen05 kernel
+    from paper_1509_03838_b200 import _device as D
+    p = nent.derive_params(3, w)
     rng = np.random.default_rng(n + K)
     c = rng.integers(-2048, 2048, (3, n), dtype=np.int64)
     g = rng.integers(-2048, 2048, (K,), dtype=np.int64)
@@ -41,6 +45,8 @@ def test_chunked_pipeline_matches_oracle(oracle, n, K, chunk, off):
         pipe.run(c_host, d_host, failed=r)
         pipe.synchronize()
         assert np.array_equal(d_host.to(torch.int64).numpy(), ref), (n, K, chunk, off, r)
+    if w == 48 and K >= 64:  # (short filters take a CUDA-core flavour)
+        assert D.last_conv_kernel() == "tcgen05_m3"
     pipe.capture(c_host, d_host, failed=2)
     d_host.fill_(-1)
     pipe.replay()

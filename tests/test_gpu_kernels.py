@@ -553,3 +553,13 @@ def test_k1_k3_vectorised_and_scalar_paths(oracle, m, w, n, off):
     mm = torch.zeros(1, dtype=torch.int64, device="cuda")
     D.extract_verify(bad, m, p.l, 0, w > 32, mm)
     assert int(mm.item()) == 1
+    # K1's fused range check: the first offender in row-major order (codec.py:34-46),
+    # in the vector body, in the ragged tail, and none
+    big = torch.zeros((m, n + 8), dtype=torch.int64, device="cuda")
+    big[:, off:off + n] = torch.from_numpy(c)
+    x = big[:, off:off + n]
+    lim = int(np.abs(c).max())
+    assert D.entangle(x, p.l, check_hi=lim)[1] is None
+    for (i, j) in ((m - 1, n - 1), (1, n // 2), (1, n // 2 + 1)):
+        x[i, j] = lim + 1
+    assert D.entangle(x, p.l, check_hi=lim)[1] == 1 * n + n // 2

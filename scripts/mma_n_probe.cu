@@ -8,15 +8,21 @@
 #include "tc05.cuh"
 using namespace nent;
 
-template <int N>
+template <int N, int MODE>
 __global__ void __launch_bounds__(128, 1) probe(int iters, long long* out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar2[8];
+  __shared__ __align__(8) uint64_t mbar3[8];  // never arrived on: parity-1 waits return at once
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) tc05::alloc(&tslot, 512);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc05::smem_u32(&mbar)));
+    for (int i = 0; i < 8; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc05::smem_u32(&mbar2[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc05::smem_u32(&mbar3[i])));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < 128 * 256 + 512; i += blockDim.x) smem[i] = (unsigned char)(i * 7 + 1);
@@ -36,8 +42,17 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, long long* out) {
       for (int it = 0; it < iters; ++it) {
         // alternate between accumulator slots like the conv kernel's ring
         const uint32_t d = tbase + 192 + (uint32_t)((it % (320 / N)) * N);
+        if (MODE >= 2) {
+          // the conv kernel's per-class hand-off: poll a barrier that is
+          // already complete (parity of the phase before the first), fence
+          uint32_t ok;
+          asm volatile("{\n .reg .pred p;\n W2_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 1;\n @!p bra W2_%=;\n selp.u32 %0, 1, 0, p;\n}"
+                       : "=r"(ok) : "r"(tc05::smem_u32(&mbar3[it & 7])) : "memory");
+          tc05::fence_after();
+        }
 #pragma unroll
         for (int kc = 0; kc < 12; ++kc) tc05::mma_i8_ts_lo(d, tbase + 8u * kc, blo + 2u * kc, idesc, kc ? 1u : 0u);
+        if (MODE >= 1) tc05::commit(tc05::smem_u32(&mbar2[it & 7]));  // (arrivals on unrelated barriers)
       }
       tc05::commit(tc05::smem_u32(&mbar));
       asm volatile(
@@ -57,18 +72,18 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, long long* out) {
   }
 }
 
-template <int N>
+template <int N, int MODE>
 void run(int iters) {
   long long* d;
   cudaMalloc(&d, 8);
   const int smem = 128 * 256 + 512 + 1024;
-  cudaFuncSetAttribute(probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<N><<<148, 128, smem>>>(64, d);
+  cudaFuncSetAttribute(probe<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe<N, MODE><<<148, 128, smem>>>(64, d);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  probe<N><<<148, 128, smem>>>(iters, d);
+  probe<N, MODE><<<148, 128, smem>>>(iters, d);
   cudaEventRecord(b);
   cudaDeviceSynchronize();
   float ms;
@@ -76,18 +91,24 @@ void run(int iters) {
   long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   const double n = (double)iters * 12;
-  printf("N=%3d: %.2f clock64-cycles per MMA, %.2f ns per MMA (event), %.1f TMAC/s chip, err=%s\n", N, h / n,
+  printf("mode %d N=%3d: %.2f clock64-cycles per MMA, %.2f ns per MMA (event), %.1f TMAC/s chip, err=%s\n", MODE, N, h / n,
          ms * 1e6 / n, n * 128.0 * N * 32 * 148 / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
   cudaFree(d);
 }
 
 int main() {
-  run<16>(4000);
-  run<32>(4000);
-  run<48>(4000);
-  run<64>(4000);
-  run<96>(4000);
-  run<128>(4000);
-  run<256>(2000);
+  run<16, 0>(4000);
+  run<32, 0>(4000);
+  run<48, 0>(4000);
+  run<64, 0>(4000);
+  run<96, 0>(4000);
+  run<128, 0>(4000);
+  run<256, 0>(2000);
+  // mode 1: a commit after every 12-step chain; mode 2: + barrier poll and fence before it
+  run<32, 1>(4000);
+  run<64, 1>(4000);
+  run<32, 2>(4000);
+  run<64, 2>(4000);
   return 0;
 }

@@ -471,7 +471,9 @@ int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
   }
   if (!(flavor & NENT_IMMA_MMA_SYNC)) {
     if (extract) {
-      const int st = tc05_fused_m3(A, np, ng, s);
+      int st = tc05_fused_m3(A, np, ng, s);
+      if (st != NENT_TC05_NA) return st;
+      st = tc05_fused_m4(A, np, ng, s);
       if (st != NENT_TC05_NA) return st;
     }
     const int st = tc05_conv(A, np, ng, extract, s);

@@ -517,6 +517,70 @@ def test_tcgen05_m3_envelope_by_sample_width(oracle):
     assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), oracle.full_conv(c2, g))
 
 
+@pytest.mark.parametrize("K", [1, 64, 257, 300, 1024, 1153])
+@pytest.mark.parametrize("n", [1, 97, 2048 - 255, 5 * 2048 + 77])
+def test_tcgen05_m4_fused_every_failure(oracle, n, K):
+    """The cfg3 hot-path kernel (conv_tc05_m4.cu: m = 4, l = 16, long filters:
+    every accumulator of a tile resident in TMEM, the Toeplitz tap operand
+    streamed through a TMEM ring) against the oracle: every failure index,
+    edge-only and multi-tile lengths, filters from one tap to the 1153-tap
+    limit, tap digits ng = 1 and 2; it must be the kernel that ran."""
+    p = nent.derive_params(4, 64)  # (4, 64, 16, 16)
+    assert (p.l, p.k) == (16, 16)
+    for bits_g, seed in ((7, 1), (10, 2)):
+        g = rand(K * 7 + seed, (K,), -(1 << bits_g), (1 << bits_g) - 1)
+        # samples as wide as int32 outputs allow (<= 0x7F7F)
+        lim = max(1, min(0x7F7F, ((1 << 31) - (1 << 16) - 1) // max(int(np.abs(g).sum()), 1)))
+        c = rand(n + K + seed, (4, n), -lim, lim)
+        ref = oracle.full_conv(c, g)
+        x = torch.from_numpy(c).cuda().to(torch.int32)
+        fl = imma_flavor(4, D.signed_digits(int(np.abs(g).max())))
+        L = n + K - 1
+        gd = D.taps_tensor(g, fl)
+        for r in (None, 0, 1, 2, 3):
+            mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+            out = torch.full((4, L), -7, dtype=torch.int32, device="cuda")
+            D.fused_conv(x, gd, K, p.l, fl, r, True, L, n_in=n, out=out, mismatch=mm if r is None else None)
+            assert D.last_conv_kernel() == "tcgen05_m4"
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref), (n, K, bits_g, r)
+            assert int(mm.item()) == 0
+
+
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_tcgen05_m4_windows_and_row_phases(oracle, off):
+    """Output windows and row bases at every 4-byte phase through the m = 4
+    kernel (rows whose 16-byte phases differ are staged from the aligned word
+    below and read shifted), and an inconsistent input is counted."""
+    n, K = 9000, 1024
+    p = nent.derive_params(4, 64)
+    c = rand(off + 80, (4, n), -512, 511)
+    g = rand(off + 81, (K,), -512, 511)
+    ref = oracle.full_conv(c, g)
+    big = torch.zeros((4, n + 8), dtype=torch.int32, device="cuda")
+    big[:, off:off + n] = torch.from_numpy(c).to(torch.int32)
+    x = big[:, off:off + n]
+    L = n + K - 1
+    fl = imma_flavor(4, 2)
+    gd = D.taps_tensor(g, fl)
+    for y0, cnt in [(0, L), (1, 5000), (2, 2049), (3, 1), (1023, 6000), (4321, L - 4321), (L - 5, 5)]:
+        for r in (None, 2):
+            mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+            out = torch.empty((4, cnt), dtype=torch.int32, device="cuda")
+            D.fused_conv(x, gd, K, p.l, fl, r, True, L, n_in=n, y_begin=y0, n_out=cnt, out=out,
+                         mismatch=mm if r is None else None)
+            assert D.last_conv_kernel() == "tcgen05_m4"
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref[:, y0:y0 + cnt]), (off, y0, cnt, r)
+            assert int(mm.item()) == 0
+    rows = [big[i, (off + i) % 4:(off + i) % 4 + n] for i in range(4)]
+    for i in range(4):
+        big[i, (off + i) % 4:(off + i) % 4 + n] = torch.from_numpy(c[i]).to(torch.int32)
+    out = torch.empty((4, L), dtype=torch.int32, device="cuda")
+    mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+    D.fused_conv(rows, gd, K, p.l, fl, None, True, L, n_in=n, out=out, mismatch=mm)
+    assert D.last_conv_kernel() == "tcgen05_m4"
+    assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref) and int(mm.item()) == 0
+
+
 @pytest.mark.parametrize("m,w", [(3, 32), (3, 48), (3, 64), (4, 64), (5, 32), (8, 32)])
 @pytest.mark.parametrize("n,off", [(7, 0), (63, 1), (1000, 0), (1001, 3), (4099, 2), (1 << 16, 0)])
 def test_k1_k3_vectorised_and_scalar_paths(oracle, m, w, n, off):

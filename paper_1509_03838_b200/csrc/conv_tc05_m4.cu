@@ -50,8 +50,25 @@ int tc05_fused_m4(ConvArgs& A, int np, int ng, cudaStream_t s) {
   void (*kern)(ConvArgs, Geom) = ng == 1 ? conv_tc05_m4_kernel<1> : conv_tc05_m4_kernel<2>;
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
+#ifdef NENT_TC05_TIMERS
+  static unsigned long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s);
+  G.dbg = dbg;
+#endif
   kern<<<grid, NT, SMEM, s>>>(A, G);
   note_conv_kernel(5);
+#ifdef NENT_TC05_TIMERS
+  {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "m4 timers (kcycles/CTA): mma wait planes %.1f taps %.1f acc_free %.1f total %.1f | tap writer wait_free %.1f"
+            " total %.1f | epi wait_full %.1f total %.1f | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid,
+            h[2] / 1e3 / grid, h[3] / 1e3 / grid, h[4] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid,
+            h[7] / 1e3 / grid, (double)G.ntiles / grid);
+  }
+#endif
   return check_launch("tc05 fused m4");
 }
 

@@ -134,6 +134,27 @@ __device__ __forceinline__ void mma_i8_ts_lo(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(SW128_DESC_HI));
 }
 
+// 64-bit SW128 descriptor from its low word, and an in-place advance of the
+// start address (16-byte units): the high word stays where it is, so a
+// descriptor walked along K costs one add per step instead of a rebuild
+__device__ __forceinline__ uint64_t desc_sw128_from_lo(uint32_t lo) {
+  uint64_t d;
+  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "n"(SW128_DESC_HI));
+  return d;
+}
+__device__ __forceinline__ void desc_advance(uint64_t& d, uint32_t units) {
+  asm volatile("{\n .reg .b32 lo, hi;\n mov.b64 {lo, hi}, %0;\n add.u32 lo, lo, %1;\n mov.b64 %0, {lo, hi};\n}"
+               : "+l"(d)
+               : "r"(units));
+}
+__device__ __forceinline__ void mma_i8_ts_desc(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 // arrive once on an mbarrier when every MMA issued so far by this thread is done
 __device__ __forceinline__ void commit(uint32_t mbar_saddr) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar_saddr)

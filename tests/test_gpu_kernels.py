@@ -518,7 +518,7 @@ def test_tcgen05_m3_envelope_by_sample_width(oracle):
 
 
 @pytest.mark.parametrize("K", [1, 64, 257, 300, 1024, 1153])
-@pytest.mark.parametrize("n", [1, 97, 2048 - 255, 5 * 2048 + 77])
+@pytest.mark.parametrize("n", [1, 97, 4096 - 255, 5 * 4096 + 77])
 def test_tcgen05_m4_fused_every_failure(oracle, n, K):
     """The cfg3 hot-path kernel (conv_tc05_m4.cu: m = 4, l = 16, long filters:
     every accumulator of a tile resident in TMEM, the Toeplitz tap operand
@@ -551,7 +551,7 @@ def test_tcgen05_m4_windows_and_row_phases(oracle, off):
     """Output windows and row bases at every 4-byte phase through the m = 4
     kernel (rows whose 16-byte phases differ are staged from the aligned word
     below and read shifted), and an inconsistent input is counted."""
-    n, K = 9000, 1024
+    n, K = 15000, 1024
     p = nent.derive_params(4, 64)
     c = rand(off + 80, (4, n), -512, 511)
     g = rand(off + 81, (K,), -512, 511)
@@ -562,7 +562,7 @@ def test_tcgen05_m4_windows_and_row_phases(oracle, off):
     L = n + K - 1
     fl = imma_flavor(4, 2)
     gd = D.taps_tensor(g, fl)
-    for y0, cnt in [(0, L), (1, 5000), (2, 2049), (3, 1), (1023, 6000), (4321, L - 4321), (L - 5, 5)]:
+    for y0, cnt in [(0, L), (1, 5000), (2, 4097), (3, 1), (1023, 6000), (4321, L - 4321), (L - 5, 5)]:
         for r in (None, 2):
             mm = torch.zeros(1, dtype=torch.int64, device="cuda")
             out = torch.empty((4, cnt), dtype=torch.int32, device="cuda")

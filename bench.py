@@ -295,6 +295,10 @@ def run_ours(args):
         plain(plain_same)
         plain(plain_fast)
     torch.cuda.synchronize(dev)
+    plain(plain_same)
+    plain_kernels = {"plain_same_kernel": D.last_conv_kernel()}
+    plain(plain_fast)
+    plain_kernels["plain_fastest"] = D.last_conv_kernel()
     fused_step()
     kernel_kind = D.last_conv_kernel()
     torch.cuda.synchronize(dev)
@@ -362,6 +366,8 @@ def run_ours(args):
         "interleaved_ms": med,
         "flavors": {"entangled": MAC_NAMES[flavor], "plain_same_kernel": MAC_NAMES[plain_same],
                     "plain_fastest": MAC_NAMES[plain_fast], "cuda_core": MAC_NAMES[core_flavor]},
+        "kernels": dict(plain_kernels, entangled=kernel_kind),
+        "plain_fastest_samples_per_s": samples_job / (b2b["plain_fastest"] / 1e3) if world == 1 else None,
     }
 
     # ---------------- measured pipe peaks (roofline denominators) ----------------

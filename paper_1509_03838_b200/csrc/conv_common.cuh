@@ -103,6 +103,7 @@ int tc05_conv(ConvArgs& A, int np, int ng, bool extract, cudaStream_t s);
 // fused m = 3 with the byte-aligned shift l = 16 (conv_tc05_m3.cu), or NENT_TC05_NA
 int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s);
 bool tc05_m3_envelope(const ConvArgs& A, int np, int ng);
+int tc05_plain_m3(ConvArgs& A, int np, int ng, cudaStream_t s);
 int tc05_fused_m4(ConvArgs& A, int np, int ng, cudaStream_t s);
 bool tc05_m4_envelope(const ConvArgs& A, int np, int ng);
 

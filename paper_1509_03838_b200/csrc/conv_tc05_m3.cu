@@ -10,6 +10,14 @@ namespace nent {
 namespace tcm3 {
 using KernFn = void (*)(ConvArgs, Geom);
 
+static KernFn plain_kernel_for(int nsteps, int ng) {
+  static const KernFn tab[3][2] = {{conv_tc05_m3_kernel<1, 4, true>, conv_tc05_m3_kernel<2, 4, true>},
+                                   {conv_tc05_m3_kernel<1, 8, true>, conv_tc05_m3_kernel<2, 8, true>},
+                                   {conv_tc05_m3_kernel<1, 12, true>, conv_tc05_m3_kernel<2, 12, true>}};
+  if (ng < 1 || ng > 2 || nsteps % 4 || nsteps < 4 || nsteps > 12) return nullptr;
+  return tab[nsteps / 4 - 1][ng - 1];
+}
+
 static KernFn kernel_for(int nsteps, int ng) {
   static const KernFn tab[3][2] = {{conv_tc05_m3_kernel<1, 4>, conv_tc05_m3_kernel<2, 4>},
                                    {conv_tc05_m3_kernel<1, 8>, conv_tc05_m3_kernel<2, 8>},
@@ -38,6 +46,32 @@ bool tc05_m3_envelope(const ConvArgs& A, int np, int ng) {
   return true;
 }
 
+// Plain (non-entangled) convolution of exactly three int16-range int32 streams
+// on the m = 3 kernel: no entangling operand, two data digits.
+bool tc05_plain_m3_envelope(const ConvArgs& A, int np, int ng) {
+  if (A.rows != 3 || A.in_bits != 32 || A.y_bits != 32 || np != 2 || ng < 1 || ng > 2) return false;
+  for (int i = 0; i < 3; ++i)
+    if (A.a.p[i] || !A.b.p[i] || !A.y.p[i]) return false;
+  if (A.perm || A.add || A.scale != 1) return false;
+  if (A.period < A.n_in + A.K - 1 && !(A.y_begin >= A.K - 1 && A.y_begin + A.n_out <= A.period)) return false;
+  if (A.K < 1 || A.K > 257) return false;
+  for (int i = 0; i < 3; ++i)
+    if (reinterpret_cast<uintptr_t>(A.b.p[i]) & 3) return false;
+  if ((int64_t)32768 * A.K * ng >= ((int64_t)1 << 31)) return false;
+  return true;
+}
+
+static int launch_m3(ConvArgs& A, int ng, bool plain, cudaStream_t s);
+
+int tc05_plain_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
+  static const bool enabled = [] {
+    const char* e = getenv("NENT_TC05_M3");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!enabled || !tc05_plain_m3_envelope(A, np, ng)) return NENT_TC05_NA;
+  return launch_m3(A, ng, true, s);
+}
+
 int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
   using namespace tcm3;
   // A/B switch for measurements (read once): NENT_TC05_M3=0 routes these
@@ -47,6 +81,11 @@ int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
     return !(e && atoi(e) == 0);
   }();
   if (!enabled || !tc05_m3_envelope(A, np, ng)) return NENT_TC05_NA;
+  return launch_m3(A, ng, false, s);
+}
+
+static int launch_m3(ConvArgs& A, int ng, bool plain, cudaStream_t s) {
+  using namespace tcm3;
   const int sms = sm100_sms();
   if (sms <= 0) return NENT_TC05_NA;
   Geom G{};
@@ -60,7 +99,7 @@ int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
   for (int i = 0; i < 3; ++i)
     G.dph[i] = (int)((((reinterpret_cast<uintptr_t>(A.b.p[i]) - reinterpret_cast<uintptr_t>(A.b.p[0])) >> 2) % 4 + 4) % 4);
   G.ntiles = (A.n_out + G.shift + TILE - 1) / TILE;
-  const KernFn kern = kernel_for(G.nsteps, ng);
+  const KernFn kern = plain ? plain_kernel_for(G.nsteps, ng) : kernel_for(G.nsteps, ng);
   if (!kern) return NENT_TC05_NA;
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);

@@ -166,19 +166,25 @@ __device__ __forceinline__ uint32_t wide1(uint32_t r1, uint32_t r0, uint32_t& q)
 __device__ __forceinline__ int32_t sar16(uint32_t x) { return (int32_t)x >> 16; }
 
 // the chains (data digit p, tap digit j) of digit class c, in a fixed order
-template <int NG, typename F>
+template <int NG, int NPD, typename F>
 __device__ __forceinline__ void for_class(int c, F&& f) {
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
+  for (int p = 0; p < NPD; ++p) {
     const int j = c - p;
     if (j >= 0 && j < NG) f(p, j);
   }
 }
 
-template <int NG, int NSTEPS>
+// PLAIN: the same kernel on three NON-entangled streams of int16-range samples
+// (the reference's apply_conventional, ops.py:241-247): two data digits per
+// stream (its own byte planes), 2 x NG chains in NG + 1 classes, and an
+// epilogue that only recombines y = sum_c R_c 256^c -- the plain convolution
+// this GPU does best, the baseline of bench.py's overhead figure.
+template <int NG, int NSTEPS, bool PLAIN = false>
 __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_constant__ ConvArgs A,
                                                              const __grid_constant__ Geom G) {
-  constexpr int NCLS = 4 + NG - 1;
+  constexpr int NPD = PLAIN ? 2 : 4;     // data digits per stream
+  constexpr int NCLS = NPD + NG - 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // plane full[NSLOT], plane empty[NSLOT], stage full[NSTAGE], stage free[NSTAGE], acc full[5], acc empty[5]
   __shared__ __align__(8) uint64_t bars[2 * NSLOT + 2 * NSTAGE + 2 * SLOTS];
@@ -337,6 +343,28 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       const int64_t ybase = tile * TILE - G.shift;
       const int64_t o0 = ybase + 128 * (EC * part) + v;
       const bool interior = ybase >= 0 && ybase + TILE <= A.n_out;
+      if constexpr (PLAIN) {
+        // three independent streams: y_i = R_0 + (R_1 << 8) + (R_2 << 16), int32
+#pragma unroll 1
+        for (int i = 0; i < 3; ++i) {
+          uint32_t acc[EC];
+          class_step(false, [&](int k, uint32_t a, uint32_t) { acc[k] = a; });
+          class_step(false, [&](int k, uint32_t a, uint32_t) { acc[k] += a << 8; });
+          if constexpr (NCLS == 3) class_step(false, [&](int k, uint32_t a, uint32_t) { acc[k] += a << 16; });
+          int32_t* y = reinterpret_cast<int32_t*>(i == 0 ? A.y.p[0] : (i == 1 ? A.y.p[1] : A.y.p[2])) + o0;
+          if (interior) {
+#pragma unroll
+            for (int k = 0; k < EC; ++k) y[128 * k] = (int32_t)acc[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < EC; ++k) {
+              const int64_t o = o0 + 128 * k;
+              if (o >= 0 && o < A.n_out) y[128 * k] = (int32_t)acc[k];
+            }
+          }
+        }
+        continue;
+      }
       // Recovery from delta_A = delta_{P+1} = (d_P << 16) + d_{P+1} and
       // delta_B = delta_{P+2} = (d_{P+1} << 16) + d_{P+2} with int32 outputs
       // (the y_bits == 32 contract), all modulo 2^32:
@@ -498,7 +526,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
             const uint32_t d = tbase + (uint32_t)(RING0 + rs * U);
             const int im1 = i == 0 ? 2 : i - 1;
             bool first = true;
-            for_class<NG>(c, [&](int p, int j) {
+            for_class<NG, NPD>(c, [&](int p, int j) {
               // data digit p of eps_i: bytes of c_i (p < 2) or of c_{i-1} (p >= 2)
               const int raw = p < 2 ? i : im1;
               const uint32_t blo0 = tc05::desc_sw128_lo(slot_s + (uint32_t)((2 * raw + (p & 1)) * PLANE));
@@ -514,14 +542,21 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
             tc05::commit(accf_b(rs));
             ++kslot;
           };
+          if constexpr (PLAIN) {
 #pragma unroll
-          for (int c = 0; c < NCLS; ++c) {
-            issue_class(sA, c);
-            issue_class(sB, c);
-          }
-          if (verify) {
+            for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int c = 0; c < NCLS; ++c) issue_class(P, c);
+              for (int c = 0; c < NCLS; ++c) issue_class(i, c);
+          } else {
+#pragma unroll
+            for (int c = 0; c < NCLS; ++c) {
+              issue_class(sA, c);
+              issue_class(sB, c);
+            }
+            if (verify) {
+#pragma unroll
+              for (int c = 0; c < NCLS; ++c) issue_class(P, c);
+            }
           }
           tc05::commit(empty_b(ts));
         }

@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -m gpu -x -p no:cacheprovider -k "m3" > gpurun_out/t_tests.log 2>&1; echo "rc=$?" >> gpurun_out/t_tests.log
+timeout 600 python bench.py --steps 50 --no-extras --no-cpu-baseline > gpurun_out/t_bench.log 2>&1; echo "rc=$?" >> gpurun_out/t_bench.log

@@ -517,6 +517,28 @@ def test_tcgen05_m3_envelope_by_sample_width(oracle):
     assert np.array_equal(res.outputs.data.to(torch.int64).cpu().numpy(), oracle.full_conv(c2, g))
 
 
+@pytest.mark.parametrize("K", [1, 64, 129, 256, 257])
+@pytest.mark.parametrize("n", [1, 97, 8192 - 255, 3 * 8192 + 77])
+def test_tcgen05_m3_plain_conv(oracle, n, K):
+    """The non-entangled convolution of three int16-range streams on the m = 3
+    kernel's plain mode (two data digits, no extraction): full convolutions and
+    output windows, tap digits ng = 1 and 2, against the oracle."""
+    for bits_g, seed in ((7, 1), (12, 2)):
+        g = rand(K * 5 + seed, (K,), -(1 << bits_g), (1 << bits_g) - 1)
+        lim = max(1, min(0x7F7F, ((1 << 31) - 1) // max(int(np.abs(g).sum()), 1)))
+        c = rand(n + K + seed, (3, n), -lim, lim)
+        ref = oracle.full_conv(c, g)
+        x = torch.from_numpy(c).cuda().to(torch.int32)
+        fl = imma_flavor(2, D.signed_digits(int(np.abs(g).max())))
+        gd = D.taps_tensor(g, fl)
+        L = n + K - 1
+        for y0, cnt in [(0, L), (min(3, L - 1), max(1, (L - 3) // 2))]:
+            out = torch.full((3, cnt), -7, dtype=torch.int32, device="cuda")
+            D.conv(x, gd, K, fl, period=L, y_begin=y0, n_out=cnt, out=out)
+            assert D.last_conv_kernel() == "tcgen05_m3"
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref[:, y0:y0 + cnt]), (n, K, bits_g, y0)
+
+
 @pytest.mark.parametrize("K", [1, 64, 257, 300, 1024, 1153])
 @pytest.mark.parametrize("n", [1, 97, 4096 - 255, 5 * 4096 + 77])
 def test_tcgen05_m4_fused_every_failure(oracle, n, K):

@@ -85,18 +85,34 @@ def entangled_conv(block: StreamBlock, g, failed: int | None = None, mode: str =
     if not 1 <= K <= n and mode == "circular":
         raise ParameterError(f"kernel length {K} not in 1..{n}")
     period = n + K - 1 if mode == "full" else n
+    g_np = g if not isinstance(g, torch.Tensor) else g.cpu().numpy()
+    mc = None
+    if flavor is None or host:
+        # the bound of the data as it sits on the device (one reduction kernel;
+        # a host pass over 2^24-sample streams would cost more than the upload)
+        mc = max_c if max_c is not None else D.max_abs(c)
     if flavor is None:
-        mc = max_c if max_c is not None else (D.host_max_abs(block.data) if host else D.max_abs(c))
-        flavor = conv_flavor(_eps_bound(mc, p), g if not isinstance(g, torch.Tensor) else g.cpu().numpy(),
-                             n_out=period)
+        flavor = conv_flavor(_eps_bound(mc, p), g_np, n_out=period)
     if flavor in (MAC_G64, MAC_X128):
         raise ParameterError("operands too wide for the fused kernel; use the staged API")
     if g_dev is None:
-        g_dev = D.taps_tensor(g if not isinstance(g, torch.Tensor) else g.cpu().numpy(), flavor)
+        g_dev = D.taps_tensor(g_np, flavor)
     if verify and failed is None and mismatch is None:
         mismatch = torch.zeros(1, dtype=torch.int64, device=c.device)
+    # Host (numpy int64) blocks: when the entangled words and the admitted output
+    # bound (ops.py:163) fit 32 bits, the device works on int32 rows -- the
+    # tensor-core kernels' operand width -- and widens the result before it
+    # goes back, so the reference-shaped call runs the same kernels as a
+    # device-resident int32 block.
+    narrow = (host and out is None and out_dtype == torch.int64 and c.dtype == torch.int64
+              and _eps_bound(mc, p) < 1 << 31 and mc * int(np.abs(g_np.astype(object)).sum()) < 1 << 31)
+    if narrow:
+        c = c.to(torch.int32)
     d = D.fused_conv(c, g_dev, K, p.l, flavor, failed, p.w > 32, period, n_in=n,
-                     out_dtype=out_dtype, out=out, mismatch=mismatch if failed is None else None)
+                     out_dtype=torch.int32 if narrow else out_dtype, out=out,
+                     mismatch=mismatch if failed is None else None)
+    if narrow:
+        d = d.to(torch.int64)
     mm = int(mismatch.item()) if (verify and failed is None) else None
     return FusedResult(_finish(p, d, host), MAC_NAMES[flavor], mm)
 

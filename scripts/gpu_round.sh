@@ -20,3 +20,9 @@ $CMD2 > gpurun_out/${TAG}_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on --warp-sampling-interval 0 -k regex:conv_tc05_m3 -s 2 -c 1 \
     -o gpurun_out/${TAG}_prof_m3 $CMD2 > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/${TAG}_plain2.log
+# the cfg3 kernel: one full capture as well
+CMD3="python scripts/m4_time.py 2"
+$CMD3 > gpurun_out/${TAG}_plain3.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:conv_tc05_m4 -s 2 -c 1 \
+    -o gpurun_out/${TAG}_prof_m4 $CMD3 > gpurun_out/${TAG}_ncu_full_m4.log 2>&1
+echo "full m4 rc=$?" >> gpurun_out/${TAG}_plain3.log

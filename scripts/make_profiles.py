@@ -62,3 +62,13 @@ if rep.exists():
             "gpc__cycles_elapsed.avg.per_second", "launch__registers_per_thread",
             "sm__inst_executed.avg.per_cycle_elapsed", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
     print({k: (val[hdr.index(k)], unit(k)) for k in keys if k in hdr})
+
+rep4 = G / f"{tag}_prof_m4.ncu-rep"
+if rep4.exists():
+    raw = subprocess.run(["ncu", "-i", str(rep4), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    (P / f"{tag}_ncu_raw_tcgen05_m4_cfg3.csv").write_text(raw)
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, val = rows[0], rows[2]
+    keys = ["gpu__time_duration.sum", "sm__cycles_elapsed.max", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "gpc__cycles_elapsed.avg.per_second"]
+    print("m4:", {k: (val[hdr.index(k)], rows[1][hdr.index(k)]) for k in keys if k in hdr})

@@ -236,6 +236,45 @@ fused_outer_kernel(const Rows c, int64_t n, int l, const TG* __restrict__ g, int
     for (int s = 0; s < MT; ++s) cv[s] = (int64_t)__ldg(reinterpret_cast<const TI*>(c.p[s]) + b * n + u);
 #pragma unroll
     for (int s = 0; s < MT; ++s) e[s] = wadd(wshl(cv[(s + MT - 1) % MT], l), cv[s]);
+    // Fast path (the cfg4 shape): entangled words and taps that fit int32 make
+    // every product one IMAD.WIDE, and int32 outputs leave as 16-byte vectors
+    // (four consecutive v per thread).  Block-uniform choice per row u.
+    bool narrow = sizeof(TG) == 4 && sizeof(TO) == 4 && (p & 3) == 0;
+#pragma unroll
+    for (int s = 0; s < MT; ++s) narrow = narrow && e[s] == (int64_t)(int32_t)e[s];
+#pragma unroll
+    for (int s = 0; s < MT; ++s)
+      narrow = narrow && (!d.p[s] || (reinterpret_cast<uintptr_t>(d.p[s]) & 15) == 0);
+    narrow = narrow && (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+    if (narrow) {
+      const int64_t base = (b * n + u) * p;
+      for (int64_t v = 4 * (int64_t)threadIdx.x; v < p; v += 4 * LT) {
+        const int4 g4 = __ldg(reinterpret_cast<const int4*>(g + v));
+        const int gq[4] = {g4.x, g4.y, g4.z, g4.w};
+        int o32[MT][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int64_t dl[MT], orot[MT];
+#pragma unroll
+          for (int s = 0; s < MT; ++s) dl[s] = (int64_t)(int32_t)e[s] * (int64_t)gq[q];
+          recover_regs_valid<MT>(dl, pivot, l, orot);
+#pragma unroll
+          for (int t = 0; t < MT; ++t) {
+            o32[t][q] = (int)(uint32_t)(uint64_t)orot[t];
+            part[t] += orot[t];
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          int row = pivot + t;
+          row -= row >= MT ? MT : 0;
+          if (d.p[row])
+            *reinterpret_cast<int4*>(reinterpret_cast<TO*>(d.p[row]) + base + v) =
+                make_int4(o32[t][0], o32[t][1], o32[t][2], o32[t][3]);
+        }
+      }
+      continue;
+    }
     for (int64_t v = threadIdx.x; v < p; v += LT) {
       const int64_t gv = (int64_t)__ldg(g + v);
       int64_t dl[MT], orot[MT];

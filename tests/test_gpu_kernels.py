@@ -361,6 +361,14 @@ def test_fused_outer(oracle):
         fused.entangled_outer(wl.params, c, g, failed=r, out=out, sums=sums)
         assert np.array_equal(out.cpu().numpy(), ref), r
         assert np.array_equal(sums.cpu().numpy(), ref.sum(axis=(2, 3))), r
+        # int32 samples and outputs: the vectorised IMAD.WIDE path (p % 4 == 0)
+        # and, with a ragged p, the general one
+        for pp in (len(g), len(g) - 1):
+            out32 = torch.empty((m, B, n, pp), dtype=torch.int32, device="cuda")
+            sums = torch.zeros((m, B), dtype=torch.int64, device="cuda")
+            fused.entangled_outer(wl.params, c.to(torch.int32), g[:pp], failed=r, out=out32, sums=sums)
+            assert np.array_equal(out32.to(torch.int64).cpu().numpy(), ref[..., :pp]), (r, pp)
+            assert np.array_equal(sums.cpu().numpy(), ref[..., :pp].sum(axis=(2, 3))), (r, pp)
 
 
 def test_extract_int32_and_peer_style_rows(oracle):

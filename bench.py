@@ -670,8 +670,11 @@ def other_configs(D, fused, dev, stream, w):
         fl = fused.conv_flavor(xb, wl.g, n_out=L)
         gd = D.taps_tensor(wl.g, fl)
         tab = D.imma_table(gd, K, fl, 0)
-        split = (chain and D.imma_kernel(fl, K, wl.m, True) != "tcgen05"
-                 and D.imma_kernel(fl, K, wl.m, False) == "tcgen05")
+        # (the fused m = 8 tcgen05 kernel takes cfg5's chain rows; NENT_BENCH_CFG5_SPLIT=1
+        # times the older plain conv + separate extract pass instead)
+        split = (chain and D.imma_kernel(fl, K, wl.m, False) == "tcgen05"
+                 and (D.imma_kernel(fl, K, wl.m, True) != "tcgen05"
+                      or os.environ.get("NENT_BENCH_CFG5_SPLIT") == "1"))
         if split:
             delta = torch.empty((wl.m, L), dtype=torch.int32, device=dev)
 

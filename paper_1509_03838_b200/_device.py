@@ -277,7 +277,7 @@ def imma_kernel(flavor: int, K: int, rows: int, extract: bool) -> str:
 
 def last_conv_kernel() -> str:
     """The convolution kernel this host thread launched last."""
-    return {0: "none", 1: "cuda-core", 2: "mma.sync", 3: "tcgen05", 4: "tcgen05_m3", 5: "tcgen05_m4"}[
+    return {0: "none", 1: "cuda-core", 2: "mma.sync", 3: "tcgen05", 4: "tcgen05_m3", 5: "tcgen05_m4", 6: "tcgen05_m8"}[
         _lib.lib().nent_last_conv_kernel()]
 
 

@@ -106,5 +106,7 @@ bool tc05_m3_envelope(const ConvArgs& A, int np, int ng);
 int tc05_plain_m3(ConvArgs& A, int np, int ng, cudaStream_t s);
 int tc05_fused_m4(ConvArgs& A, int np, int ng, cudaStream_t s);
 bool tc05_m4_envelope(const ConvArgs& A, int np, int ng);
+int tc05_fused_m8(ConvArgs& A, int np, int ng, cudaStream_t s);
+bool tc05_m8_envelope(const ConvArgs& A, int np, int ng);
 
 }  // namespace nent

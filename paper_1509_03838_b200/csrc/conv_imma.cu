@@ -475,6 +475,8 @@ int imma_dispatch(ConvArgs& A, int flavor, bool extract, cudaStream_t s) {
       if (st != NENT_TC05_NA) return st;
       st = tc05_fused_m4(A, np, ng, s);
       if (st != NENT_TC05_NA) return st;
+      st = tc05_fused_m8(A, np, ng, s);
+      if (st != NENT_TC05_NA) return st;
     } else {
       const int st = tc05_plain_m3(A, np, ng, s);
       if (st != NENT_TC05_NA) return st;

@@ -137,5 +137,12 @@ extern "C" int nent_imma_kernel(int flavor, int K, int rows, int extract) {
   if (flavor & NENT_IMMA_MMA_SYNC) return 1;
   tcc::Geom G;
   size_t smem = 0;
-  return tc05_geometry(K, rows, (flavor >> 8) & 0xf, (flavor >> 12) & 0xf, extract != 0, G, smem) ? 2 : 1;
+  const int np = (flavor >> 8) & 0xf, ng = (flavor >> 12) & 0xf;
+  // the dedicated fused kernels (int32 rows, byte-aligned digits): m = 4 long
+  // filters (conv_tc05_m4) and m = 8 already-entangled rows (conv_tc05_m8)
+  if (extract && sm100_sms() > 0) {
+    if (rows == 4 && np == 4 && ng <= 2 && K <= 1153) return 2;
+    if (rows == 8 && np == 2 && ng == 1 && K <= 257) return 2;
+  }
+  return tc05_geometry(K, rows, np, ng, extract != 0, G, smem) ? 2 : 1;
 }

@@ -195,7 +195,18 @@ def entangled_chain_conv(block: StreamBlock, scale: int, add, perm, g, failed: i
         # record read per permuted position (int32 indices when they fit)
         perm_idx = perm_dev.to(torch.int32) if n < (1 << 31) else perm_dev
         x = D.gather_records(D.interleave_chain(c.to(torch.int32), p.l, scale, add_ent), perm_idx)
-        if (is_imma(flavor) and D.imma_kernel(flavor, K, m, True) != "tcgen05"
+        sum_g = int(np.abs(g.astype(object)).sum())
+        d_bound = (mc * abs(int(scale)) + D.max_abs(add_dev.reshape(1, -1))) * sum_g  # ops.py:163
+        if (is_imma(flavor) and D.imma_kernel(flavor, K, m, True) == "tcgen05" and m > 3
+                and d_bound < 1 << 31):
+            # the fused tcgen05 kernels for m > 3 work on int32 rows (the
+            # recovered outputs fit them: admitted bound < 2^31): conv + extract
+            # in one pass, delta never reaches HBM
+            d = D.fused_conv(x, g_dev, K, p.l, flavor, failed, p.w > 32, L, n_in=n,
+                             out_dtype=torch.int32, mismatch=mismatch, pre_entangled=True)
+            if out_dtype != torch.int32:
+                d = d.to(out_dtype)
+        elif (is_imma(flavor) and D.imma_kernel(flavor, K, m, True) != "tcgen05"
                 and D.imma_kernel(flavor, K, m, False) == "tcgen05"):
             # m > 3: the fused tensor-core kernel would be the mma.sync one; the
             # tcgen05 kernel convolves the m chain rows (the workers' entangled

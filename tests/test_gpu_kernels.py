@@ -280,9 +280,9 @@ def test_chain_conv_cfg5_shape(oracle):
 
 @pytest.mark.parametrize("mma_sync", [False, True])
 def test_chain_conv_cfg5_tensor_core_routes(oracle, mma_sync):
-    """cfg5's chain on the tensor cores: the fused mma.sync kernel, or (m = 8 is
-    outside the fused tcgen05 envelope) the tcgen05 conv of the chain rows
-    followed by the verifying extract pass -- same outputs, same check."""
+    """cfg5's chain on the tensor cores: the fused mma.sync kernel, or the fused
+    m = 8 tcgen05 kernel (conv + extract of the chain rows in one pass) -- same
+    outputs, same check."""
     from paper_1509_03838_b200 import workloads
     wl = workloads.make(5, n=3 * 8192 + 500)
     x = (wl.c * wl.scale + wl.add)[:, wl.perm]
@@ -293,8 +293,45 @@ def test_chain_conv_cfg5_tensor_core_routes(oracle, mma_sync):
         res = fused.entangled_chain_conv(nent.StreamBlock(wl.params, wl.c), wl.scale, wl.add,
                                          wl.perm, wl.g, failed=r, flavor=fl)
         assert np.array_equal(res.outputs.data, ref), (mma_sync, r)
+        assert D.last_conv_kernel() == ("mma.sync" if mma_sync else "tcgen05_m8")
         if r is None:
             assert res.mismatches == 0
+
+
+@pytest.mark.parametrize("K", [1, 64, 128, 129, 257])
+@pytest.mark.parametrize("n", [1, 97, 4096 - 127, 3 * 4096 + 77])
+def test_tcgen05_m8_fused_every_failure(oracle, n, K):
+    """The cfg5 convolution stage (conv_tc05_m8.cu: eight already-entangled
+    int32 rows, convolution + recovery in one pass): every failure index and
+    the redundant-row check, edge-only and multi-tile lengths, every tap-table
+    size, output windows; an inconsistent row is counted."""
+    p = nent.derive_params(8, 32)  # (8, 32, 4, 4)
+    g = rand(K * 3 + 1, (K,), -127, 127)
+    lim = max(1, min(120, (nent.output_range(p).hi - 1) // max(int(np.abs(g).sum()), 1)))
+    c = rand(n + K, (8, n), -lim, lim)
+    ref = oracle.full_conv(c, g)
+    eps = oracle.entangle(c, p.l)
+    assert np.abs(eps).max() <= 0x7F7F
+    x = torch.from_numpy(eps).cuda().to(torch.int32)
+    fl = imma_flavor(2, 1)
+    gd = D.taps_tensor(g, fl)
+    L = n + K - 1
+    for r in (None, 0, 3, 7):
+        for y0, cnt in [(0, L), (min(5, L - 1), max(1, (L - 5) // 2))]:
+            mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+            out = torch.full((8, cnt), -7, dtype=torch.int32, device="cuda")
+            D.fused_conv(x, gd, K, p.l, fl, r, False, L, n_in=n, y_begin=y0, n_out=cnt, out=out,
+                         mismatch=mm if r is None else None, pre_entangled=True)
+            assert D.last_conv_kernel() == "tcgen05_m8"
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref[:, y0:y0 + cnt]), (n, K, r, y0)
+            assert int(mm.item()) == 0
+    if n > 50:
+        bad = x.clone()
+        bad[0, n // 2] += 1  # the redundant row no longer matches the other seven
+        mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = torch.empty((8, L), dtype=torch.int32, device="cuda")
+        D.fused_conv(bad, gd, K, p.l, fl, None, False, L, n_in=n, out=out, mismatch=mm, pre_entangled=True)
+        assert int(mm.item()) > 0
 
 
 def test_extract_verify_counts_inconsistent_words(oracle):

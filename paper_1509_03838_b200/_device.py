@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes
 
+import os
+
 import numpy as np
 import torch
 
@@ -29,6 +31,71 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+# ---- large host arrays: pinned staging + threaded host copies ---------------
+# The reference API hands numpy int64 arrays in and expects them back.  A
+# pageable cudaMemcpy of a 2^24-sample block runs at a few GB/s and the fresh
+# result array is page-faulted in by one thread, which together cost far more
+# than the kernels.  Blocks of STAGE_MIN bytes and more go through one cached
+# pinned buffer per direction instead: the host-side copy into / out of it is
+# split over a few threads (numpy releases the GIL for large copies) and the
+# DMA runs at PCIe rate.
+STAGE_MIN = 8 << 20
+STAGE_MAX = 2 << 30
+_stage = {}          # direction -> pinned uint8 tensor
+_stage_pool = None
+
+
+def _pool():
+    global _stage_pool
+    if _stage_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _stage_pool = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    return _stage_pool
+
+
+def _staging(direction: str, nbytes: int) -> torch.Tensor:
+    buf = _stage.get(direction)
+    if buf is None or buf.numel() < nbytes:
+        _stage[direction] = buf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    return buf[:nbytes]
+
+
+def _threaded_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[...] = src for two C-contiguous arrays of one dtype, in parallel slabs."""
+    d, s = dst.reshape(-1), src.reshape(-1)
+    n = d.size
+    parts = min(8, max(1, n // (1 << 20)))
+    step = -(-n // parts)
+    list(_pool().map(lambda i: np.copyto(d[i * step:(i + 1) * step], s[i * step:(i + 1) * step]), range(parts)))
+
+
+def host_to_device(arr: np.ndarray, dev) -> torch.Tensor:
+    """C-contiguous int32/int64 numpy array -> device tensor."""
+    if not STAGE_MIN <= arr.nbytes <= STAGE_MAX:
+        return torch.from_numpy(arr).to(dev)
+    tdt = torch.from_numpy(arr[:0]).dtype
+    stage = _staging("in", arr.nbytes).view(tdt).reshape(arr.shape)  # pinned
+    _threaded_copy(stage.numpy(), arr)
+    t = torch.empty(arr.shape, dtype=tdt, device=dev)
+    t.copy_(stage, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()  # the staging buffer may be refilled by the next call
+    return t
+
+
+def device_to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> a fresh numpy array (what ``t.cpu().numpy()`` returns)."""
+    nbytes = t.numel() * t.element_size()
+    if not t.is_cuda or not STAGE_MIN <= nbytes <= STAGE_MAX:
+        return t.cpu().numpy()
+    stage = _staging("out", nbytes).view(t.dtype).reshape(t.shape)  # pinned
+    stage.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    src = stage.numpy()
+    out = np.empty(src.shape, dtype=src.dtype)
+    _threaded_copy(out, src)
+    return out
+
+
 def as_device(data, dtype=torch.int64) -> torch.Tensor:
     """Host numpy / tensor -> CUDA tensor (2-D rows contiguous)."""
     dev = device()
@@ -38,7 +105,7 @@ def as_device(data, dtype=torch.int64) -> torch.Tensor:
             t = t.to(torch.int64)
         return t if dtype is None else t.to(dtype)
     arr = np.ascontiguousarray(data, dtype=np.int64)
-    t = torch.from_numpy(arr).to(dev)
+    t = host_to_device(arr, dev)
     return t if dtype in (None, torch.int64) else t.to(dtype)
 
 

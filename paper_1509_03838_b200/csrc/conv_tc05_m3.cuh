@@ -66,6 +66,9 @@ constexpr int NCONV = 6;               // converter warps
 // Warp ids: the schedulers favour higher warp ids.  Default: epilogue 0-7,
 // converters 8-13, loader 14, MMA issuer 15.  NENT_M3_EPI_HIGH puts the
 // epilogue (the role with the most instructions) in warps 8-15 instead.
+#ifndef NENT_M3_WALK
+#define NENT_M3_WALK 0
+#endif
 #ifndef NENT_M3_EPI_HIGH
 #define NENT_M3_EPI_HIGH 0
 #endif
@@ -533,9 +536,28 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
               const uint32_t a = tbase + (uint32_t)(8 * j * NSTEPS);
               const uint32_t idesc = (p & 1) ? idesc_s : idesc_u;
 #ifndef NENT_M3_DBG_NOMMA
+#if NENT_M3_WALK
+              // operands walked in place through a run-time loop of 4-MMA groups:
+              // the descriptor and the tap address are loop-carried, so they stay
+              // in the uniform datapath (one add each per MMA, no vector -> uniform moves)
+              uint64_t bd = tc05::desc_sw128_from_lo(blo0);
+              uint32_t ak = a;
+              uint32_t accf = first ? 0u : 1u;
+#pragma unroll 1
+              for (int kq = 0; kq < NSTEPS / 4; ++kq) {
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4) {
+                  tc05::mma_i8_ts_desc(d, ak, bd, idesc, (k4 == 0) ? accf : 1u);
+                  tc05::desc_advance(bd, 2u);
+                  ak += 8u;
+                }
+                accf = 1u;
+              }
+#else
 #pragma unroll
               for (int kc = 0; kc < NSTEPS; ++kc)
                 tc05::mma_i8_ts_lo(d, a + 8u * kc, blo0 + 2u * kc, idesc, (first && kc == 0) ? 0u : 1u);
+#endif
 #endif
               first = false;
             });

@@ -61,7 +61,7 @@ def _prep(block: StreamBlock, dtype=None) -> tuple[torch.Tensor, bool]:
 
 
 def _finish(p, d: torch.Tensor, host: bool) -> StreamBlock:
-    return StreamBlock(p, d.cpu().numpy() if host else d)
+    return StreamBlock(p, D.device_to_host(d) if host else d)
 
 
 def entangled_conv(block: StreamBlock, g, failed: int | None = None, mode: str = "full",

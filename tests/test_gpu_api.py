@@ -277,3 +277,27 @@ def test_inplace_int32_device_block_wide_words():
     b32 = nent.StreamBlock(p32, torch.from_numpy(small).cuda().to(torch.int32))
     ent32 = nent.entangle_inplace(b32)
     assert np.array_equal(ent32.data.cpu().numpy(), nent.entangle(nent.StreamBlock(p32, small)).data)
+
+
+def test_large_host_blocks_use_pinned_staging(oracle):
+    """numpy int64 blocks above the staging threshold go through the cached
+    pinned buffers (threaded host copies, DMA at PCIe rate): results equal the
+    oracle's, and the array a call returned is not touched by the next call."""
+    from paper_1509_03838_b200 import _device as D
+    from paper_1509_03838_b200 import fused
+    p = nent.derive_params(3, 48)
+    n = (1 << 20) + 3
+    assert 3 * n * 8 >= D.STAGE_MIN
+    rng = np.random.default_rng(11)
+    g = rng.integers(-2048, 2048, (64,), dtype=np.int64)
+    c1 = rng.integers(-2048, 2048, (3, n), dtype=np.int64)
+    c2 = rng.integers(-2048, 2048, (3, n), dtype=np.int64)
+    r1 = fused.entangled_conv(nent.StreamBlock(p, c1), g)
+    keep = r1.outputs.data.copy()
+    r2 = fused.entangled_conv(nent.StreamBlock(p, c2), g, failed=1)
+    assert np.array_equal(r1.outputs.data, keep) and np.array_equal(keep, oracle.full_conv(c1, g))
+    assert np.array_equal(r2.outputs.data, oracle.full_conv(c2, g))
+    assert r1.outputs.data.dtype == np.int64 and r1.mismatches == 0
+    t = torch.arange(3 * n, dtype=torch.int64, device="cuda").reshape(3, n)
+    assert np.array_equal(D.device_to_host(t), t.cpu().numpy())
+    assert torch.equal(D.host_to_device(keep, t.device).cpu(), torch.from_numpy(keep))

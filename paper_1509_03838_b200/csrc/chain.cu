@@ -31,9 +31,12 @@ struct ChainArgs {
   int add_bits;
 };
 
-template <typename T, bool CHAIN = false>
-__global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m, int64_t n, T* __restrict__ out,
+// MT > 0 fixes the stream count at compile time (MT = 8: the record index
+// arithmetic of the store loop is shifts instead of run-time divisions).
+template <typename T, bool CHAIN = false, int MT = 0>
+__global__ void __launch_bounds__(256) interleave_kernel(const Rows x, int m_rt, int64_t n, T* __restrict__ out,
                                                          const ChainArgs ch = ChainArgs{}) {
+  const int m = MT > 0 ? MT : m_rt;
   constexpr int P = 4096 / sizeof(T);        // positions per tile (1024 int32, 512 int64)
   constexpr int V = 16 / sizeof(T);          // elements per 16-byte vector
   __shared__ T tile[8][P + 16 / sizeof(T)];  // padded rows
@@ -227,7 +230,8 @@ int nent_interleave_chain(const void* const* x, int x_bits, int m, int64_t n, in
   const ChainArgs ch{l, scale, add, add_bits};
   const int grid = grid_for(n, x_bits == 32 ? 1024 : 512, 1, 148 * 8);
   cudaStream_t s = as_stream(stream);
-  if (x_bits == 32) interleave_kernel<int32_t, true><<<grid, 256, 0, s>>>(R, m, n, (int32_t*)out, ch);
+  if (x_bits == 32 && m == 8) interleave_kernel<int32_t, true, 8><<<grid, 256, 0, s>>>(R, m, n, (int32_t*)out, ch);
+  else if (x_bits == 32) interleave_kernel<int32_t, true><<<grid, 256, 0, s>>>(R, m, n, (int32_t*)out, ch);
   else interleave_kernel<int64_t, true><<<grid, 256, 0, s>>>(R, m, n, (int64_t*)out, ch);
   return check_launch("interleave_chain");
 }

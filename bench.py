@@ -431,7 +431,10 @@ def run_ours(args):
     if world in (4, 8) and not args.no_extras:
         del d_dev, y_plain
         torch.cuda.empty_cache()
-        spg = run_stream_per_gpu(3 if world == 4 else 5, min(args.steps, 20), args.warmup, dev, backend)
+        try:  # an extra: a failure here must not cost the halo-split headline line
+            spg = run_stream_per_gpu(3 if world == 4 else 5, min(args.steps, 20), args.warmup, dev, backend)
+        except Exception as exc:  # pragma: no cover - multi-GPU only
+            spg = {"error": f"{type(exc).__name__}: {str(exc)[:300]}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

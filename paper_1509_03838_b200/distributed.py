@@ -197,8 +197,8 @@ class StreamPerGPU:
         recv = send.new_empty(sum(recv_sizes))
         dist.all_to_all_single(recv, send.reshape(-1), recv_sizes, send_sizes, group=self.group)
         recv = recv.to(delta_local.device)
-        if not me_alive:
-            return delta_local.new_empty((m, 0)), 0, 0
+        if not me_alive:  # (the recovered slices are int64 on every rank: gather() needs one dtype)
+            return torch.empty((m, 0), dtype=torch.int64, device=delta_local.device), 0, 0
         width = me - mb
         rows = [None] * m
         off = 0
@@ -312,8 +312,9 @@ class PeerRows:
 
         m = self.drv.world
         mb, me = self.bounds(failed)
-        if me == mb:
-            return self.local.new_empty((m, 0)), 0, 0
+        if me == mb:  # the failed rank: an empty slice of the dtype the survivors produce
+            return torch.empty((m, 0), dtype=out.dtype if out is not None else torch.int64,
+                               device=self.local.device), 0, 0
         r = 0 if failed is None else failed  # failed=None pivots on stream 0 (codec.py:49-51)
         rows = [None if (j == r or t is None) else t[mb:me] for j, t in enumerate(self.rows)]
         if out is None:

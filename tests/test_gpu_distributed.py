@@ -66,6 +66,15 @@ def _stream_worker(rank, world, port, cfg, n, K, failures, q):
                 out = drv.gather(d, int(delta.shape[-1]), failed, dst=0)
                 if rank == 0:
                     got[(failed, how)] = out.to(torch.int64).cpu().numpy()
+            if cfg == 5 and failed is not None:
+                # int32 delta buffers (the bench's): the failed rank's empty slice
+                # must have the dtype the survivors' recovered slices have
+                d32 = delta.to(torch.int32)
+                for how in ("all_to_all", "peer"):
+                    d, b, e = (drv.recover if how == "all_to_all" else drv.recover_peer)(d32, failed)
+                    out = drv.gather(d, int(delta.shape[-1]), failed, dst=0)
+                    if rank == 0:
+                        got[(failed, how + "_int32")] = out.to(torch.int64).cpu().numpy()
         if rank == 0:
             full = n is None
             if full:

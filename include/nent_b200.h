@@ -62,8 +62,11 @@ extern "C" {
 int nent_imma_kernel(int flavor, int K, int rows, int extract);
 /* The convolution kernel the calling host thread launched last (diagnostic,
  * for tests and the benchmark): 1 CUDA-core tile kernel, 2 mma.sync digit
- * slicing, 3 tcgen05 digit slicing, 4 tcgen05 fused m = 3 with l = 16
- * (conv_tc05_m3.cu), 0 none yet. */
+ * slicing, 3 tcgen05 digit slicing (generic), 4 tcgen05 m = 3 kernel with
+ * l = 16 (conv_tc05_m3.cu: fused, or its plain mode for three non-entangled
+ * streams), 5 tcgen05 fused m = 4 long-filter kernel (conv_tc05_m4.cu),
+ * 6 tcgen05 fused m = 8 kernel on already-entangled rows (conv_tc05_m8.cu),
+ * 0 none yet. */
 int nent_last_conv_kernel(void);
 
 /* Elementwise op codes (ops.py:193-204). */

@@ -248,20 +248,29 @@ fused_outer_kernel(const Rows c, int64_t n, int l, const TG* __restrict__ g, int
     narrow = narrow && (reinterpret_cast<uintptr_t>(g) & 15) == 0;
     if (narrow) {
       const int64_t base = (b * n + u) * p;
+      // the m-1 surviving entangled words in rotation order, once per row u
+      // (the pivot's product is never formed, as in the reference's recovery)
+      int32_t erot[MT - 1];
+#pragma unroll
+      for (int t = 0; t < MT - 1; ++t) {
+        int idx = pivot + 1 + t;
+        idx -= idx >= MT ? MT : 0;
+        erot[t] = (int32_t)select_mod<MT>(e, idx);
+      }
       for (int64_t v = 4 * (int64_t)threadIdx.x; v < p; v += 4 * LT) {
         const int4 g4 = __ldg(reinterpret_cast<const int4*>(g + v));
         const int gq[4] = {g4.x, g4.y, g4.z, g4.w};
         int o32[MT][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          int64_t dl[MT], orot[MT];
+          int64_t rot[MT - 1], orot[MT];
 #pragma unroll
-          for (int s = 0; s < MT; ++s) dl[s] = (int64_t)(int32_t)e[s] * (int64_t)gq[q];
-          recover_regs_valid<MT>(dl, pivot, l, orot);
+          for (int t = 0; t < MT - 1; ++t) rot[t] = (int64_t)erot[t] * (int64_t)gq[q];
+          recover_rot_valid<MT>(rot, l, orot);
 #pragma unroll
           for (int t = 0; t < MT; ++t) {
             o32[t][q] = (int)(uint32_t)(uint64_t)orot[t];
-            part[t] += orot[t];
+            if (sums) part[t] += orot[t];
           }
         }
 #pragma unroll

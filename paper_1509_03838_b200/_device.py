@@ -9,8 +9,8 @@ except where a status word must be read back (range check, overflow count).
 from __future__ import annotations
 
 import ctypes
-
 import os
+import threading
 
 import numpy as np
 import torch
@@ -43,6 +43,7 @@ STAGE_MIN = 8 << 20
 STAGE_MAX = 2 << 30
 _stage = {}          # direction -> pinned uint8 tensor
 _stage_pool = None
+_stage_lock = {"in": threading.Lock(), "out": threading.Lock()}  # one user of a staging buffer at a time
 
 
 def _pool():
@@ -74,11 +75,12 @@ def host_to_device(arr: np.ndarray, dev) -> torch.Tensor:
     if not STAGE_MIN <= arr.nbytes <= STAGE_MAX:
         return torch.from_numpy(arr).to(dev)
     tdt = torch.from_numpy(arr[:0]).dtype
-    stage = _staging("in", arr.nbytes).view(tdt).reshape(arr.shape)  # pinned
-    _threaded_copy(stage.numpy(), arr)
-    t = torch.empty(arr.shape, dtype=tdt, device=dev)
-    t.copy_(stage, non_blocking=True)
-    torch.cuda.current_stream(dev).synchronize()  # the staging buffer may be refilled by the next call
+    with _stage_lock["in"]:
+        stage = _staging("in", arr.nbytes).view(tdt).reshape(arr.shape)  # pinned
+        _threaded_copy(stage.numpy(), arr)
+        t = torch.empty(arr.shape, dtype=tdt, device=dev)
+        t.copy_(stage, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()  # the staging buffer may be refilled by the next call
     return t
 
 
@@ -87,12 +89,13 @@ def device_to_host(t: torch.Tensor) -> np.ndarray:
     nbytes = t.numel() * t.element_size()
     if not t.is_cuda or not STAGE_MIN <= nbytes <= STAGE_MAX:
         return t.cpu().numpy()
-    stage = _staging("out", nbytes).view(t.dtype).reshape(t.shape)  # pinned
-    stage.copy_(t, non_blocking=True)
-    torch.cuda.current_stream(t.device).synchronize()
-    src = stage.numpy()
-    out = np.empty(src.shape, dtype=src.dtype)
-    _threaded_copy(out, src)
+    with _stage_lock["out"]:
+        stage = _staging("out", nbytes).view(t.dtype).reshape(t.shape)  # pinned
+        stage.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        src = stage.numpy()
+        out = np.empty(src.shape, dtype=src.dtype)
+        _threaded_copy(out, src)
     return out
 
 

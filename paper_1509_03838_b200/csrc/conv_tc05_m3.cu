@@ -72,6 +72,28 @@ int tc05_plain_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
   return launch_m3(A, ng, true, s);
 }
 
+
+// CTA b processes the tiles (tile_off + b + k * grid) mod ntiles.  The stream-edge tiles
+// (tile 0 and the last ones, whose windows do not lie wholly inside the streams and are
+// loaded element by element) are the slow ones; the offset places that run on the CTAs that
+// have one tile fewer than the others when the tile count is not a multiple of the grid.
+static int64_t edge_tile_offset(const ConvArgs& A, const tcm3::Geom& G, unsigned grid) {
+  using namespace tcm3;
+  const int64_t nt = G.ntiles;
+  const int64_t rem = nt % grid;
+  if (nt <= (int64_t)grid || rem == 0) return 0;
+  // first tile whose window reaches past the end of the streams
+  const int64_t base = A.y_begin - G.shift - (G.KT - 128);  // tile 0's first input sample
+  int64_t e0 = (A.n_in - 4 * (int64_t)NWP - 4 - base) / TILE + 1;  // smallest idx with base + idx TILE + 4 NWP + 4 > n_in
+  if (A.n_in - 4 * (int64_t)NWP - 4 - base < 0) e0 = 0;
+  if (e0 > nt) e0 = nt;
+  if (e0 < 1) e0 = 1;
+  const int64_t run = (nt - e0) + 1;  // tiles e0 .. nt-1, then tile 0
+  int64_t j0 = (int64_t)grid - run;   // the run ends on the last CTA
+  if (j0 < rem) j0 = rem;             // (longer than the short CTAs: start at the first of them)
+  return (((e0 - j0) % nt) + nt) % nt;
+}
+
 int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
   using namespace tcm3;
   // A/B switch for measurements (read once): NENT_TC05_M3=0 routes these
@@ -103,19 +125,29 @@ static int launch_m3(ConvArgs& A, int ng, bool plain, cudaStream_t s) {
   if (!kern) return NENT_TC05_NA;
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
-#ifdef NENT_TC05_TIMERS
+  G.tile_off = edge_tile_offset(A, G, grid);
+#if defined(NENT_TC05_TIMERS) || defined(NENT_M3_STAMPS)
+  // profiling builds: role timers (NENT_TC05_TIMERS, printed after every launch) and / or the
+  // per-CTA timeline stamps (NENT_M3_STAMPS: launches stay back to back, the last launch's
+  // timeline is printed when NENT_M3_DUMP is set in the environment)
   static unsigned long long* dbg = nullptr;
-  if (!dbg) cudaMalloc(&dbg, 64 * sizeof(unsigned long long));
-  cudaMemsetAsync(dbg, 0, 64 * sizeof(unsigned long long), s);
+  if (!dbg) cudaMalloc(&dbg, (64 + 16 * 160) * sizeof(unsigned long long));
+#ifdef NENT_TC05_TIMERS
+  cudaMemsetAsync(dbg, 0, (64 + 16 * 160) * sizeof(unsigned long long), s);
+  const bool dump = true;
+#else
+  const bool dump = getenv("NENT_M3_DUMP") != nullptr;
+#endif
   G.dbg = dbg;
 #endif
   kern<<<grid, NT, SMEM, s>>>(A, G);
   note_conv_kernel(4);
-#ifdef NENT_TC05_TIMERS
-  {
-    unsigned long long h[64];
+#if defined(NENT_TC05_TIMERS) || defined(NENT_M3_STAMPS)
+  if (dump) {
+    static unsigned long long h[64 + 16 * 160];
     cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+#ifdef NENT_TC05_TIMERS
     fprintf(stderr, "m3 timers (kcycles/CTA): mma wait_full %.1f wait_acce %.1f total %.1f | loader wait_free %.1f total %.1f"
             " | epi wait_accf %.1f total %.1f | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid,
             h[3] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[8] / 1e3 / grid, (double)G.ntiles / grid);
@@ -124,11 +156,51 @@ static int launch_m3(ConvArgs& A, int ng, bool plain, cudaStream_t s) {
     fprintf(stderr, "\n  epilogue wait per step (AB0..AB4, P01, P23, P4):");
     for (int k = 0; k < 8; ++k) fprintf(stderr, " %.1f", h[48 + k] / 1e3 / grid);
     fprintf(stderr, "\n");
+#endif
+    {
+      static const char* names[14] = {"entry", "alloc+sync", "taps built", "first planes", "2nd tile's planes", "last tile's planes",
+                                      "last MMA issued", "MMAs done", "epilogue done", "exit", "conv0: window 0 in", "conv0: window 1 in",
+                                      "conv0: window 2 in", "conv0: tile 0 done"};
+      unsigned long long t0 = ~0ull;
+      for (unsigned c = 0; c < grid; ++c) t0 = h[64 + 16 * c] < t0 ? h[64 + 16 * c] : t0;
+      fprintf(stderr, "  timeline over %u CTAs, us from the first entry (min / mean / max [CTA]):\n", grid);
+      for (int k = 0; k < 14; ++k) {
+        double mn = 1e30, mx = -1, sum = 0;
+        unsigned arg = 0;
+        for (unsigned c = 0; c < grid; ++c) {
+          const double v = (double)(h[64 + 16 * c + k] - t0) / 1e3;
+          sum += v;
+          if (v < mn) mn = v;
+          if (v > mx) mx = v, arg = c;
+        }
+        fprintf(stderr, "    %-20s %8.2f %8.2f %8.2f [%u]\n", names[k], mn, sum / grid, mx, arg);
+      }
+      {
+        double f = 0;
+        for (unsigned c = 0; c < grid; ++c)
+          f += (double)(h[64 + 16 * c + 15] - h[64 + 16 * c + 14]) / (double)(h[64 + 16 * c + 9] - h[64 + 16 * c + 0]);
+        fprintf(stderr, "    effective SM clock over the kernel: %.3f GHz\n", f / grid);
+      }
+      // per-tile-count classes
+      for (int cls = 0; cls < 2; ++cls) {
+        double mx = -1, sum = 0; int cnt = 0;
+        const long long full = (G.ntiles + grid - 1) / grid;
+        for (unsigned c = 0; c < grid; ++c) {
+          const long long mt = G.ntiles > c ? (G.ntiles - 1 - c) / grid + 1 : 0;
+          if ((mt == full) != (cls == 0)) continue;
+          const double v = (double)(h[64 + 16 * c + 9] - t0) / 1e3;
+          sum += v; ++cnt; if (v > mx) mx = v;
+        }
+        if (cnt) fprintf(stderr, "    exit of the %d CTAs with %lld tiles: mean %.2f max %.2f\n", cnt, cls == 0 ? full : full - 1, sum / cnt, mx);
+      }
+    }
+#ifdef NENT_TC05_TIMERS
     for (int w = 0; w < 2; ++w) {
       const unsigned long long* q = h + 16 + 8 * w;
       fprintf(stderr, "  converter warp %d: wait_empty %.1f wait_stage %.1f convert+sts %.1f total %.1f\n", w,
               q[0] / 1e3 / grid, q[1] / 1e3 / grid, q[4] / 1e3 / grid, q[6] / 1e3 / grid);
     }
+#endif
   }
 #endif
   return check_launch("tc05 fused m3");

@@ -77,6 +77,7 @@ constexpr int CONV0 = NENT_M3_EPI_HIGH ? 0 : 8;  // first converter warp
 constexpr int LOAD_WARP = CONV0 + NCONV;
 constexpr int MMA_WARP = LOAD_WARP + 1;
 constexpr int NT = 32 * 16;
+constexpr int TAPBAR = 32 * (NEPI + NCONV + 1);  // named barrier 2: tap builders arrive, converters and the MMA warp wait
 constexpr int EC = U / (NEPI / 4);     // 32 accumulator columns per epilogue thread
 // A raw stream's window of a tile is TILE + 256 samples (the K <= 257 halo) =
 // NWP int4 words, staged by ONE bulk copy; converter warp cw owns words
@@ -84,7 +85,7 @@ constexpr int EC = U / (NEPI / 4);     // 32 accumulator columns per epilogue th
 constexpr int WW = 11;                 // int4 words per lane and raw-stream window
 constexpr int NWP = WW * 32 * NCONV;   // 2112 int4 = 8448 samples
 #ifndef NENT_M3_NSTAGE
-#define NENT_M3_NSTAGE 2
+#define NENT_M3_NSTAGE 3
 #endif
 #ifndef NENT_M3_NSLOT
 #define NENT_M3_NSLOT 2
@@ -105,15 +106,17 @@ constexpr int EPI_REGS = NENT_M3_EPI_REGS, PROD_REGS = 256 - EPI_REGS;
 static_assert(EPI_REGS % 8 == 0 && PROD_REGS >= 40, "setmaxnreg granularity");
 static_assert(NEPI * 32 * EPI_REGS + (NT / 32 - NEPI) * 32 * PROD_REGS <= NT * LAUNCH_REGS, "launch register pool");
 static_assert(NEPI % 4 == 0 && (NT / 32 - NEPI) % 4 == 0, "setmaxnreg acts on whole warpgroups");
+static_assert(NSLOT >= 2, "the taps' digits are staged in the last plane slot while the first tile is split into slot 0");
 static_assert(4 * NWP >= TILE + 256, "a staged window covers the tile plus the K <= 257 halo");
 static_assert(4 * NWP <= PLANE, "a staged window fits its plane");
 constexpr uint32_t SSTR = WINB + 128;  // staging slot stride: a window plus one int4 of lead-in
-constexpr size_t SMEM = NSLOT * (size_t)SLOTB + (size_t)NSTAGE * SSTR;  // 178,432 B at NSTAGE = 2
+constexpr size_t SMEM = NSLOT * (size_t)SLOTB + (size_t)NSTAGE * SSTR;  // 212,352 B at NSTAGE = 3
 static_assert(SMEM + 1024 <= 227 * 1024, "shared memory");
 
 struct Geom {
   int KT, nsteps;
   int64_t ntiles;
+  int64_t tile_off;  // CTA b's tiles are (tile_off + b + k * grid) mod ntiles (conv_tc05_m3.cu: edge_tile_offset)
   int shift;   // tiles start `shift` outputs early: row 0's windows are 16-byte aligned
   int dph[3];  // word phase of row s relative to row 0 (mod 4): its windows are
                // copied from dph[s] words earlier and read shifted in shared memory
@@ -135,6 +138,21 @@ struct Geom {
   { __VA_ARGS__; }
 #define TM_BEGIN()
 #define TM_END(i)
+#endif
+#if defined(NENT_TC05_TIMERS) || defined(NENT_M3_STAMPS)
+// STAMP(i): every CTA records the global timer (ns) at point i of its timeline
+#define STAMP(i)                                                          \
+  if (G.dbg) {                                                            \
+    unsigned long long gt_;                                               \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                \
+    G.dbg[64 + 16 * blockIdx.x + (i)] = gt_;                              \
+  }
+// STAMPC(i): the SM's cycle counter at the same kind of point (effective clock = cycles / ns)
+#define STAMPC(i) \
+  if (G.dbg) G.dbg[64 + 16 * blockIdx.x + (i)] = (unsigned long long)clock64();
+#else
+#define STAMP(i)
+#define STAMPC(i)
 #endif
 
 // bytes 0 (unsigned low digit) and 1 (signed high digit) of 4 consecutive
@@ -204,6 +222,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
   auto accf_b = [&](int s) { return bar0 + 8u * (uint32_t)(B0 + 2 * NSTAGE + s); };
   auto acce_b = [&](int s) { return bar0 + 8u * (uint32_t)(B0 + 2 * NSTAGE + SLOTS + s); };
 
+  if (tid == 0) STAMP(0);
+  if (tid == 0) STAMPC(14);
   if (tid == 0) {
     for (int s = 0; s < NSLOT; ++s) {
       mb_init(full_b(s), NCONV);  // one arrival per converter warp and tile
@@ -224,11 +244,21 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
   __syncthreads();
   tc05::fence_after();
   if (tmem_slot != 0 || (planes_s & 1023u)) __trap();
+  if (tid == 0) STAMP(1);
   constexpr uint32_t tbase = 0;
   const int my_tiles = G.ntiles > blockIdx.x ? (int)((G.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  // The CTA's tiles (tile_off + blockIdx.x + k * gridDim.x) mod ntiles are processed in the
+  // order k = 1, 2, ..., 0.  The stream-edge tiles (tile 0 and the last ones), whose windows
+  // are loaded element by element, are the slow ones: tile_off puts them on the CTAs with one
+  // tile fewer where it can, and a CTA's k = 0 tile comes last so that an edge tile is never
+  // the first one (nothing overlaps a first tile's loads).
+  auto tile_ord = [&](int t) -> int64_t {
+    int64_t j = G.tile_off + blockIdx.x + (int64_t)(t + 1 < my_tiles ? t + 1 : 0) * gridDim.x;
+    return j >= G.ntiles ? j - G.ntiles : j;
+  };
   // the first input sample of this CTA's t-th tile's windows (row 0's phase)
-  const int64_t P0_first = A.y_begin - G.shift + (int64_t)blockIdx.x * TILE - (G.KT - 128);
-  const int64_t P0_step = (int64_t)gridDim.x * TILE;
+  auto P0_of = [&](int t) -> int64_t { return A.y_begin - G.shift + tile_ord(t) * TILE - (G.KT - 128); };
+  const int64_t P0_first = P0_of(0);
   // a tile is staged by TMA iff its whole window lies inside the streams
   auto staged = [&](int64_t P0) { return P0 >= 4 && P0 + 4 * (int64_t)NWP + 4 <= A.n_in; };
   // one raw window: row s from dph[s] words earlier, so every source is 16-byte aligned
@@ -246,35 +276,6 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
 #pragma unroll
     for (int s = 0; s < PRE; ++s) issue_window(s, P0_first, s);
   }
-  {
-    // the reversed taps' digits, staged once in the (still free) last plane slot:
-    // rev[j][i] = digit_j(g[KT-1-i]), A_j[v][k] = rev[j][k - v + 127]
-    const int RL = G.KT + 128;
-    unsigned char* rev = smem_raw + (NSLOT - 1) * SLOTB;
-    const uint64_t gbias = bias_of(NG);
-    for (int i = tid; i < RL; i += NT) {
-      const int idx = G.KT - 1 - i;
-      const int64_t gv = (idx >= 0 && idx < A.K) ? ld_bits(A.g, A.g_bits, idx) : 0;
-      const uint64_t d = digits_of(gv, gbias);
-      for (int j = 0; j < NG; ++j) rev[j * RL + i] = (unsigned char)(d >> (8 * j));
-    }
-    __syncthreads();
-    const int v = 32 * (warp & 3) + lane;
-    for (int blk = warp >> 2; blk < NG * NSTEPS; blk += NT / 128) {
-      const int j = blk / NSTEPS, kc = blk % NSTEPS;
-      const unsigned char* r = rev + j * RL + 32 * kc - v + 127;
-      uint32_t w[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        w[c] = (uint32_t)r[4 * c] | ((uint32_t)r[4 * c + 1] << 8) | ((uint32_t)r[4 * c + 2] << 16) |
-               ((uint32_t)r[4 * c + 3] << 24);
-      tc05::st_x8(tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 8u * (uint32_t)blk, w);
-    }
-    tc05::wait_st();
-    tc05::fence_before();
-    __syncthreads();  // also: the taps' staging bytes are dead before a converter writes that plane slot
-    tc05::fence_after();
-  }
   const bool verify = A.r < 0;
   const int P = verify ? 0 : A.r;  // pivot: the stream never read (or checked last)
   const int sA = P + 1 >= 3 ? P - 2 : P + 1, sB = P + 2 >= 3 ? P - 1 : P + 2;
@@ -288,6 +289,41 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
 
   if (warp >= EPI0 && warp < EPI0 + NEPI) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
+    {
+      // ---------------- tap table ----------------
+      // Built by the epilogue warps while the converters split the first tile.
+      // The reversed taps' digits are staged once in the (still free) last plane
+      // slot: rev[j][i] = digit_j(g[KT-1-i]), A_j[v][k] = rev[j][k - v + 127].
+      const int RL = G.KT + 128;
+      unsigned char* rev = smem_raw + (NSLOT - 1) * SLOTB;
+      const uint64_t gbias = bias_of(NG);
+      for (int i = tid - 32 * EPI0; i < RL; i += 32 * NEPI) {
+        const int idx = G.KT - 1 - i;
+        const int64_t gv = (idx >= 0 && idx < A.K) ? ld_bits(A.g, A.g_bits, idx) : 0;
+        const uint64_t d = digits_of(gv, gbias);
+        for (int j = 0; j < NG; ++j) rev[j * RL + i] = (unsigned char)(d >> (8 * j));
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
+      const int v = 32 * (warp & 3) + lane;
+      for (int blk = (warp - EPI0) >> 2; blk < NG * NSTEPS; blk += NEPI / 4) {
+        const int j = blk / NSTEPS, kc = blk % NSTEPS;
+        // lane v's 32 bytes start at byte a of the staged digits: 9 aligned words, 8 byte selects
+        const uint32_t a = (uint32_t)(j * RL + 32 * kc - v + 127);
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(rev) + (a >> 2);
+        const uint32_t sel = 0x3210u + 0x1111u * (a & 3u);
+        uint32_t x[9], w[8];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) x[c] = q[c];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) w[c] = __byte_perm(x[c], x[c + 1], sel);
+        tc05::st_x8(tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 8u * (uint32_t)blk, w);
+      }
+      tc05::wait_st();
+      tc05::fence_before();
+      // the MMA warp waits here before its first MMA, the converters before they
+      // overwrite the staged digits (their first write into the last plane slot)
+      asm volatile("bar.arrive 2, %0;" ::"n"(TAPBAR) : "memory");
+    }
     // ---------------- epilogue ----------------
     const int quad = warp & 3, part = (warp - EPI0) >> 2;
     const uint32_t lrow = (uint32_t)(32 * quad) << 16;
@@ -342,7 +378,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     int32_t* yA = reinterpret_cast<int32_t*>(A.y.p[sA]);
     int32_t* yB = reinterpret_cast<int32_t*>(A.y.p[sB]);
     for (int t = 0; t < my_tiles; ++t) {
-      const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
+      const int64_t tile = tile_ord(t);
       const int64_t ybase = tile * TILE - G.shift;
       const int64_t o0 = ybase + 128 * (EC * part) + v;
       const bool interior = ybase >= 0 && ybase + TILE <= A.n_out;
@@ -501,10 +537,16 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       const uint32_t idesc_u = tc05::idesc_i8(128, U, /*b_signed=*/false);
       const uint32_t idesc_s = tc05::idesc_i8(128, U, /*b_signed=*/true);
       int kslot = 0;
+      asm volatile("bar.sync 2, %0;" ::"n"(TAPBAR) : "memory");  // the tap table is in TMEM
+      tc05::fence_after();
+      if (lane == 0) STAMP(2);
       for (int t = 0; t < my_tiles; ++t) {
         const int ts = t % NSLOT;
         TM(0, mb_wait(full_b(ts), (uint32_t)((t / NSLOT) & 1)));
         tc05::fence_after();
+        if (t == 0 && lane == 0) STAMP(3);
+        if (t == 1 && lane == 0) STAMP(4);
+        if (t == my_tiles - 1 && lane == 0) STAMP(5);
         if (elect_one()) {
 #ifdef NENT_TC05_TIMERS
           int kpos = 0;
@@ -586,16 +628,18 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       }
       // drain the last tiles' commits before the CTA can exit: an mbarrier
       // arrive still in flight must not land in a successor CTA's shared memory
+      if (lane == 0) STAMP(6);
       for (int t = my_tiles > NSLOT ? my_tiles - NSLOT : 0; t < my_tiles; ++t)
         mb_wait(empty_b(t % NSLOT), (uint32_t)((t / NSLOT) & 1));
+      if (lane == 0) STAMP(7);
     } else if (warp == LOAD_WARP) {
       // ---------------- loader ----------------
       // One thread: every staged tile's three raw windows, one bulk copy each,
       // as soon as a staging buffer is free (the first PRE went out above).
       if (lane == 0) {
-        int64_t P0 = P0_first;
         int issued = 0;
-        for (int t = 0; t < my_tiles; ++t, P0 += P0_step) {
+        for (int t = 0; t < my_tiles; ++t) {
+          const int64_t P0 = P0_of(t);
           if (!staged(P0)) continue;
 #pragma unroll
           for (int s = 0; s < 3; ++s) {
@@ -614,11 +658,13 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       const int wbase = cw * WW * 32;
       // swizzled plane offset of this lane's word i
       auto soff = [&](int i) { return tc05::sw128(4u * (uint32_t)(wbase + 32 * i + lane)); };
-      int64_t P0 = P0_first;
       int consumed = 0;
-      for (int t = 0; t < my_tiles; ++t, P0 += P0_step) {
+      for (int t = 0; t < my_tiles; ++t) {
+        const int64_t P0 = P0_of(t);
         const int ts = t % NSLOT;
         const bool fast = staged(P0);
+        // the tap builders are done with the digits staged in the last plane slot
+        if (t == NSLOT - 1) asm volatile("bar.sync 2, %0;" ::"n"(TAPBAR) : "memory");
         // the MMAs that read this plane slot NSLOT tiles ago are done
         if (t >= NSLOT) TM(0, mb_wait_sleep(empty_b(ts), (uint32_t)(((t / NSLOT) - 1) & 1)));
 #pragma unroll 1
@@ -627,6 +673,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
           if (fast) {
             const int b = consumed % NSTAGE;
             TM(1, mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1)));
+            if (t == 0 && cw == 0 && lane == 0) STAMP(10 + s);
             const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
             const int d = dph_of(s);
             {
@@ -671,18 +718,28 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
             if (lane == 0) mb_arrive(sfree_b(b));
             ++consumed;
           } else {
+            // a stream-edge tile: element loads with zero extension, in the same two batches
             const int32_t* bp = row_of(s);
+            constexpr int BW = (WW + 1) / 2;
 #pragma unroll
-            for (int i = 0; i < WW; ++i) {
-              const int64_t q0 = P0 + 4 * (int64_t)(wbase + 32 * i + lane);
-              int e[4];
+            for (int i0 = 0; i0 < WW; i0 += BW) {
+              int e[BW][4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) e[k] = (q0 + k >= 0 && q0 + k < A.n_in) ? __ldg(bp + q0 + k) : 0;
-              uint32_t lo, hi;
-              split2(make_int4(e[0], e[1], e[2], e[3]), lo, hi);
-              const uint32_t off = soff(i);
-              sts32(plo + off, lo);
-              sts32(plo + (uint32_t)PLANE + off, hi);
+              for (int i = 0; i < BW; ++i)
+                if (i0 + i < WW) {
+                  const int64_t q0 = P0 + 4 * (int64_t)(wbase + 32 * (i0 + i) + lane);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) e[i][k] = (q0 + k >= 0 && q0 + k < A.n_in) ? __ldg(bp + q0 + k) : 0;
+                }
+#pragma unroll
+              for (int i = 0; i < BW; ++i)
+                if (i0 + i < WW) {
+                  uint32_t lo, hi;
+                  split2(make_int4(e[i][0], e[i][1], e[i][2], e[i][3]), lo, hi);
+                  const uint32_t off = soff(i0 + i);
+                  sts32(plo + off, lo);
+                  sts32(plo + (uint32_t)PLANE + off, hi);
+                }
             }
           }
         }
@@ -690,7 +747,9 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
         fence_async_smem();  // this thread's plane writes -> the MMA's async-proxy reads
         __syncwarp();
         if (lane == 0) mb_arrive(full_b(ts));
+        if (t == 0 && cw == 0 && lane == 0) STAMP(13);
       }
+      if (my_tiles < NSLOT) asm volatile("bar.sync 2, %0;" ::"n"(TAPBAR) : "memory");
     }
   }
 #ifdef NENT_TC05_TIMERS
@@ -713,8 +772,11 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
 #endif
   (void)tw;
   (void)tstart;
+  if (warp == EPI0 && lane == 0) STAMP(8);
   tc05::fence_before();
   __syncthreads();
+  if (tid == 0) STAMP(9);
+  if (tid == 0) STAMPC(15);
   if (warp == MMA_WARP) {
     tc05::fence_after();
     tc05::dealloc(tbase, 512);

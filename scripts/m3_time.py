@@ -11,7 +11,10 @@ from paper_1509_03838_b200 import _device as D  # noqa: E402
 from paper_1509_03838_b200 import workloads  # noqa: E402
 from paper_1509_03838_b200._lib import imma_flavor  # noqa: E402
 
+import os  # noqa: E402
+
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+dump = "--dump" in sys.argv  # stamps builds (-DNENT_M3_STAMPS): print the timeline of one more back-to-back launch
 wl = workloads.make(2)
 n, K = wl.n, wl.K
 L = n + K - 1
@@ -30,5 +33,9 @@ for r in (None, 1):
     for _ in range(reps):
         f()
     e1.record()
+    if dump:
+        os.environ["NENT_M3_DUMP"] = "1"
+        f()
+        del os.environ["NENT_M3_DUMP"]
     torch.cuda.synchronize()
     print("failed", r, "kernel", D.last_conv_kernel(), "ms", round(e0.elapsed_time(e1) / reps, 4), flush=True)

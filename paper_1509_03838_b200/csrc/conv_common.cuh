@@ -109,4 +109,24 @@ bool tc05_m4_envelope(const ConvArgs& A, int np, int ng);
 int tc05_fused_m8(ConvArgs& A, int np, int ng, cudaStream_t s);
 bool tc05_m8_envelope(const ConvArgs& A, int np, int ng);
 
+// Tile order of the persistent tcgen05 kernels (conv_tc05_m3 / _m4): CTA b processes the
+// tiles (tile_off + b + k * grid) mod ntiles.  The stream-edge tiles (tile 0 and the last
+// ones, whose input windows do not lie wholly inside the streams) take the slow loading
+// path; the offset places that run on the CTAs that have one tile fewer than the others
+// when the tile count is not a multiple of the grid.  `base` is tile 0's first input
+// sample, `win` the samples one window copy reads, `tile` the outputs per tile.
+inline int64_t edge_tile_offset(int64_t n_in, int64_t base, int64_t win, int64_t tile, int64_t nt, unsigned grid) {
+  const int64_t rem = nt % grid;
+  if (nt <= (int64_t)grid || rem == 0) return 0;
+  // first tile whose window reaches past the end of the streams: base + idx * tile + win > n_in
+  const int64_t room = n_in - win - base;
+  int64_t e0 = room < 0 ? 0 : room / tile + 1;
+  if (e0 > nt) e0 = nt;
+  if (e0 < 1) e0 = 1;
+  const int64_t run = (nt - e0) + 1;  // tiles e0 .. nt-1, then tile 0
+  int64_t j0 = (int64_t)grid - run;   // the run ends on the last CTA
+  if (j0 < rem) j0 = rem;             // (longer than the short CTAs: start at the first of them)
+  return (((e0 - j0) % nt) + nt) % nt;
+}
+
 }  // namespace nent

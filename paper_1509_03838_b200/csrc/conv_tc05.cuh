@@ -268,6 +268,39 @@ __device__ __forceinline__ void cp_async4_zfill(uint32_t dst, const void* src, u
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
+// One warp stages a stream-edge window with cp.async at phase 0: the nw4 int4s of `row`
+// that start at sample P0, zeros outside [0, n_in).  int4 k holds samples P0 + 4k .. + 3:
+// zero fill for k < kz0 and k >= kc (wholly outside the stream), one 16-byte copy for
+// ka <= k < kb (wholly inside; `aligned` = row + P0 is 16-byte aligned), sample by sample
+// for the at most two cut int4s in between and for every int4 of a row at another phase.
+// The caller waits (cp.async.wait_all), syncs the warp and arrives on the window's barrier.
+__device__ __forceinline__ void stage_edge_window(uint32_t dst0, const int32_t* row, int64_t P0, int64_t n_in,
+                                                  int nw4, bool aligned, int lane) {
+  auto clampw = [&](int64_t v) { return (int)(v < 0 ? 0 : (v > nw4 ? nw4 : v)); };
+  const int kz0 = clampw(P0 < 0 ? (-P0) / 4 : 0), ka = clampw(P0 < 0 ? (-P0 + 3) / 4 : 0);
+  const int64_t rest = n_in - P0;  // samples from the window's start to the stream's end
+  const int kb0 = clampw(rest < 0 ? 0 : rest / 4), kc = clampw(rest < 0 ? 0 : (rest + 3) / 4);
+  const int kb = kb0 < ka ? ka : kb0;
+  for (int k4 = lane; k4 < kz0; k4 += 32) cp_async16_zfill(dst0 + 16u * (uint32_t)k4, row, 0u);
+  for (int k4 = kc + lane; k4 < nw4; k4 += 32) cp_async16_zfill(dst0 + 16u * (uint32_t)k4, row, 0u);
+  auto by_sample = [&](int k4) {
+    const int64_t q0 = P0 + 4 * (int64_t)k4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool in = q0 + k >= 0 && q0 + k < n_in;
+      cp_async4_zfill(dst0 + 16u * (uint32_t)k4 + 4u * (uint32_t)k, in ? row + q0 + k : row, in ? 4u : 0u);
+    }
+  };
+  if (aligned) {
+    const int32_t* src = row + P0;
+    for (int k4 = ka + lane; k4 < kb; k4 += 32) cp_async16(dst0 + 16u * (uint32_t)k4, src + 4 * k4);
+    for (int k4 = kz0 + lane; k4 < ka; k4 += 32) by_sample(k4);
+    for (int k4 = kb + lane; k4 < kc; k4 += 32) by_sample(k4);
+  } else {
+    for (int k4 = kz0 + lane; k4 < kc; k4 += 32) by_sample(k4);
+  }
+}
+
 // How a tile's input window is staged: 1 = every word in range (plain
 // cp.async), 2 = partly outside [0, n_in) in full (zero-padded) mode
 // (cp.async with zero fill; words straddling 0 or n_in element by element),

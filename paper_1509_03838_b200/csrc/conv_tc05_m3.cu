@@ -73,27 +73,6 @@ int tc05_plain_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
 }
 
 
-// CTA b processes the tiles (tile_off + b + k * grid) mod ntiles.  The stream-edge tiles
-// (tile 0 and the last ones, whose windows do not lie wholly inside the streams and are
-// loaded element by element) are the slow ones; the offset places that run on the CTAs that
-// have one tile fewer than the others when the tile count is not a multiple of the grid.
-static int64_t edge_tile_offset(const ConvArgs& A, const tcm3::Geom& G, unsigned grid) {
-  using namespace tcm3;
-  const int64_t nt = G.ntiles;
-  const int64_t rem = nt % grid;
-  if (nt <= (int64_t)grid || rem == 0) return 0;
-  // first tile whose window reaches past the end of the streams
-  const int64_t base = A.y_begin - G.shift - (G.KT - 128);  // tile 0's first input sample
-  int64_t e0 = (A.n_in - 4 * (int64_t)NWP - 4 - base) / TILE + 1;  // smallest idx with base + idx TILE + 4 NWP + 4 > n_in
-  if (A.n_in - 4 * (int64_t)NWP - 4 - base < 0) e0 = 0;
-  if (e0 > nt) e0 = nt;
-  if (e0 < 1) e0 = 1;
-  const int64_t run = (nt - e0) + 1;  // tiles e0 .. nt-1, then tile 0
-  int64_t j0 = (int64_t)grid - run;   // the run ends on the last CTA
-  if (j0 < rem) j0 = rem;             // (longer than the short CTAs: start at the first of them)
-  return (((e0 - j0) % nt) + nt) % nt;
-}
-
 int tc05_fused_m3(ConvArgs& A, int np, int ng, cudaStream_t s) {
   using namespace tcm3;
   // A/B switch for measurements (read once): NENT_TC05_M3=0 routes these
@@ -125,7 +104,7 @@ static int launch_m3(ConvArgs& A, int ng, bool plain, cudaStream_t s) {
   if (!kern) return NENT_TC05_NA;
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
-  G.tile_off = edge_tile_offset(A, G, grid);
+  G.tile_off = edge_tile_offset(A.n_in, A.y_begin - G.shift - (G.KT - 128), 4 * (int64_t)NWP + 4, TILE, G.ntiles, grid);
 #if defined(NENT_TC05_TIMERS) || defined(NENT_M3_STAMPS)
   // profiling builds: role timers (NENT_TC05_TIMERS, printed after every launch) and / or the
   // per-CTA timeline stamps (NENT_M3_STAMPS: launches stay back to back, the last launch's

@@ -648,38 +648,8 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
             if (whole) {
               if (lane == 0) issue_window(s, P0, b);
             } else {
-              // int4 k of the window holds samples P0 + 4k .. P0 + 4k + 3: zeros for k < kz0 and
-              // k >= kc (wholly outside the stream), one copy for ka <= k < kb (wholly inside),
-              // sample by sample for the at most two cut int4s in between
-              const int32_t* row = reinterpret_cast<const int32_t*>(A.b.p[s]);
-              const uint32_t dst0 = stage_s + (uint32_t)b * SSTR;
-              const bool aligned = G.dph[s] == 0;  // row + P0 is 16-byte aligned
-              auto clampw = [](int64_t v) { return (int)(v < 0 ? 0 : (v > NWP ? NWP : v)); };
-              const int kz0 = clampw(P0 < 0 ? (-P0) / 4 : 0), ka = clampw(P0 < 0 ? (-P0 + 3) / 4 : 0);
-              const int64_t rest = A.n_in - P0;  // samples from the window's start to the stream's end
-              const int kb0 = clampw(rest < 0 ? 0 : rest / 4), kc = clampw(rest < 0 ? 0 : (rest + 3) / 4);
-              const int kb = kb0 < ka ? ka : kb0;
-              for (int k4 = lane; k4 < kz0; k4 += 32) tcc::cp_async16_zfill(dst0 + 16u * (uint32_t)k4, row, 0u);
-              for (int k4 = kc + lane; k4 < NWP; k4 += 32) tcc::cp_async16_zfill(dst0 + 16u * (uint32_t)k4, row, 0u);
-              if (aligned) {
-                const int32_t* src = row + P0;
-                for (int k4 = ka + lane; k4 < kb; k4 += 32) tcc::cp_async16(dst0 + 16u * (uint32_t)k4, src + 4 * k4);
-              }
-              // the cut int4s (and every int4 of a row at another 16-byte phase), sample by sample
-              auto by_sample = [&](int k4) {
-                const int64_t q0 = P0 + 4 * (int64_t)k4;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const bool in = q0 + k >= 0 && q0 + k < A.n_in;
-                  tcc::cp_async4_zfill(dst0 + 16u * (uint32_t)k4 + 4u * (uint32_t)k, in ? row + q0 + k : row, in ? 4u : 0u);
-                }
-              };
-              if (aligned) {
-                for (int k4 = kz0 + lane; k4 < ka; k4 += 32) by_sample(k4);
-                for (int k4 = kb + lane; k4 < kc; k4 += 32) by_sample(k4);
-              } else {
-                for (int k4 = kz0 + lane; k4 < kc; k4 += 32) by_sample(k4);
-              }
+              tcc::stage_edge_window(stage_s + (uint32_t)b * SSTR, reinterpret_cast<const int32_t*>(A.b.p[s]), P0, A.n_in,
+                                     NWP, G.dph[s] == 0, lane);
             }
           }
           ++issued;

@@ -50,10 +50,15 @@ int tc05_fused_m4(ConvArgs& A, int np, int ng, cudaStream_t s) {
   void (*kern)(ConvArgs, Geom) = ng == 1 ? conv_tc05_m4_kernel<1> : conv_tc05_m4_kernel<2>;
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
-#ifdef NENT_TC05_TIMERS
+  G.tile_off = edge_tile_offset(A.n_in, A.y_begin - G.shift - (G.KT - 128), 4 * (int64_t)G.nw4 + 4, TILE, G.ntiles, grid);
+#if defined(NENT_TC05_TIMERS) || defined(NENT_M4_STAMPS)
+  // profiling builds: role timers (NENT_TC05_TIMERS) / per-CTA timeline stamps (NENT_M4_STAMPS,
+  // printed for the launch made while NENT_M4_DUMP is set in the environment)
   static unsigned long long* dbg = nullptr;
-  if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
+  if (!dbg) cudaMalloc(&dbg, (16 + 8 * 160) * sizeof(unsigned long long));
+#ifdef NENT_TC05_TIMERS
   cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s);
+#endif
   G.dbg = dbg;
 #endif
   kern<<<grid, NT, SMEM, s>>>(A, G);
@@ -67,6 +72,43 @@ int tc05_fused_m4(ConvArgs& A, int np, int ng, cudaStream_t s) {
             " total %.1f | epi wait_full %.1f total %.1f | tiles/CTA %.2f\n", h[0] / 1e3 / grid, h[1] / 1e3 / grid,
             h[2] / 1e3 / grid, h[3] / 1e3 / grid, h[4] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid,
             h[7] / 1e3 / grid, (double)G.ntiles / grid);
+  }
+#endif
+#ifdef NENT_M4_STAMPS
+  if (getenv("NENT_M4_DUMP")) {
+    static unsigned long long h[16 + 8 * 160];
+    cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    static const char* names[5] = {"entry", "first planes", "2nd tile's planes", "last tile's planes", "exit"};
+    unsigned long long t0 = ~0ull;
+    for (unsigned c = 0; c < grid; ++c) t0 = h[16 + 8 * c] < t0 ? h[16 + 8 * c] : t0;
+    fprintf(stderr, "  m4 timeline over %u CTAs (%.2f tiles/CTA), us from the first entry (min / mean / max [CTA]):\n", grid,
+            (double)G.ntiles / grid);
+    for (int k = 0; k < 5; ++k) {
+      double mn = 1e30, mx = -1, sum = 0;
+      unsigned arg = 0;
+      for (unsigned c = 0; c < grid; ++c) {
+        const double v = (double)(h[16 + 8 * c + k] - t0) / 1e3;
+        sum += v;
+        if (v < mn) mn = v;
+        if (v > mx) mx = v, arg = c;
+      }
+      fprintf(stderr, "    %-20s %8.2f %8.2f %8.2f [%u]\n", names[k], mn, sum / grid, mx, arg);
+    }
+    const long long full = (G.ntiles + grid - 1) / grid;
+    for (int cls = 0; cls < 2; ++cls) {
+      double mx = -1, sum = 0;
+      int cnt = 0;
+      for (unsigned c = 0; c < grid; ++c) {
+        const long long mt = G.ntiles > c ? (G.ntiles - 1 - c) / grid + 1 : 0;
+        if ((mt == full) != (cls == 0)) continue;
+        const double v = (double)(h[16 + 8 * c + 4] - t0) / 1e3;
+        sum += v;
+        ++cnt;
+        if (v > mx) mx = v;
+      }
+      if (cnt) fprintf(stderr, "    exit of the %d CTAs with %lld tiles: mean %.2f max %.2f\n", cnt, cls == 0 ? full : full - 1, sum / cnt, mx);
+    }
   }
 #endif
   return check_launch("tc05 fused m4");

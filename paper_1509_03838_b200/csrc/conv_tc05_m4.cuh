@@ -49,6 +49,10 @@
 #include "conv_tc05_m3.cuh"
 
 namespace nent {
+#ifndef NENT_M4_WINBAR
+#define NENT_M4_WINBAR 0  // 1: the MMA starts a stream as soon as its two windows are split (measured slower: 0.1137 vs 0.1095 ms on cfg3)
+#endif
+
 namespace tcm4 {
 
 using tcc::bias_of;
@@ -84,7 +88,10 @@ constexpr int BUFC = NCLS5 * U;        // 160 columns per stream buffer
 constexpr int PLANE = 6144;            // bytes per byte plane: 128 * (U - 1) + KTMAX = 5248, 1024-aligned
 constexpr int SLOTB = 2 * M * PLANE;   // one tile slot: 4 raw streams x {lo, hi}
 constexpr int NSLOT = 2;
-constexpr int NSTAGE = 3;
+#ifndef NENT_M4_NSTAGE
+#define NENT_M4_NSTAGE 4
+#endif
+constexpr int NSTAGE = NENT_M4_NSTAGE;  // staging ring depth: a whole tile's four raw windows in flight
 constexpr uint32_t SSTR = 4 * (128 * (U - 1) + KTMAX) + 128;  // staging stride: the largest window + lead-in
 constexpr int NCOPY = 16;              // byte-shifted copies of the reversed tap digits
 constexpr int RLMAX = KTMAX + 144;     // one copy: KT + 128 bytes + one 16-byte vector of slack
@@ -98,29 +105,46 @@ struct Geom {
   int KT, nsteps, ngrp;  // GEMM K (bytes), K steps, tap-ring groups per stream pair
   int nw4;               // int4 words per raw window: (TILE + KT - 128) / 4
   int64_t ntiles;
+  int64_t tile_off;      // CTA b's tiles are (tile_off + b + k * grid) mod ntiles
   int shift;             // tiles start `shift` outputs early: row 0's windows are 16-byte aligned
   int dph[M];            // word phase of row s relative to row 0 (mod 4)
   unsigned long long* dbg;  // role timers (profiling builds, -DNENT_TC05_TIMERS)
 };
 
+// STAMP(i): every CTA records the global timer (ns) at point i of its timeline (-DNENT_M4_STAMPS)
+#ifdef NENT_M4_STAMPS
+#define M4_STAMP(i)                                           \
+  if (G.dbg) {                                                \
+    unsigned long long gt_;                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));    \
+    G.dbg[16 + 8 * blockIdx.x + (i)] = gt_;                   \
+  }
+#else
+#define M4_STAMP(i)
+#endif
+
 template <int NG>
 __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_constant__ ConvArgs A,
                                                              const __grid_constant__ Geom G) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // plane full/empty [NSLOT], stage full/free [NSTAGE], tap full/free [TRING], acc full/free [2]
-  __shared__ __align__(8) uint64_t bars[2 * NSLOT + 2 * NSTAGE + 2 * TRING + 4];
+  // plane full [NSLOT][M] / empty [NSLOT], stage full/free [NSTAGE], tap full/free [TRING], acc full/free [2]
+  __shared__ __align__(8) uint64_t bars[NSLOT * M + NSLOT + 2 * NSTAGE + 2 * TRING + 4];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) M4_STAMP(0);
   const uint32_t planes_s = tc05::smem_u32(smem_raw);
   const uint32_t stage_s = planes_s + (uint32_t)(NSLOT * SLOTB);
   unsigned char* rev = smem_raw + NSLOT * SLOTB + NSTAGE * SSTR;
   const uint32_t bar0 = tc05::smem_u32(bars);
   auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
-  auto full_b = [&](int s) { return bar(s); };
-  auto empty_b = [&](int s) { return bar(NSLOT + s); };
-  auto sfull_b = [&](int s) { return bar(2 * NSLOT + s); };
-  auto sfree_b = [&](int s) { return bar(2 * NSLOT + NSTAGE + s); };
-  constexpr int B1 = 2 * NSLOT + 2 * NSTAGE;
+  // (one "planes full" barrier per tile slot AND raw window: the MMA starts a stream as soon
+  // as the two windows it reads are split, not when the whole tile is)
+  auto full_b = [&](int ts, int s) { return bar(ts * M + s); };
+  constexpr int B0 = NSLOT * M;
+  auto empty_b = [&](int s) { return bar(B0 + s); };
+  auto sfull_b = [&](int s) { return bar(B0 + NSLOT + s); };
+  auto sfree_b = [&](int s) { return bar(B0 + NSLOT + NSTAGE + s); };
+  constexpr int B1 = B0 + NSLOT + 2 * NSTAGE;
   auto tfull_b = [&](int s) { return bar(B1 + s); };
   auto tfree_b = [&](int s) { return bar(B1 + TRING + s); };
   auto afull_b = [&](int h) { return bar(B1 + 2 * TRING + h); };
@@ -128,7 +152,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
 
   if (tid == 0) {
     for (int s = 0; s < NSLOT; ++s) {
-      mb_init(full_b(s), NCONV);
+      for (int w = 0; w < M; ++w) mb_init(full_b(s, w), NCONV);
       mb_init(empty_b(s), 1);
     }
     for (int s = 0; s < NSTAGE; ++s) {
@@ -147,8 +171,17 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
   }
   if (warp == MMA_WARP) tc05::alloc(&tmem_slot, 512);
   const int my_tiles = G.ntiles > blockIdx.x ? (int)((G.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  const int64_t P0_first = A.y_begin - G.shift + (int64_t)blockIdx.x * TILE - (G.KT - 128);
-  const int64_t P0_step = (int64_t)gridDim.x * TILE;
+  // The CTA's tiles (tile_off + blockIdx.x + k * gridDim.x) mod ntiles are processed in the
+  // order k = 1, 2, ..., 0.  The stream-edge tiles (tile 0 and the last ones), whose windows
+  // are loaded element by element, are the slow ones: tile_off (conv_tc05_m3.cu:
+  // edge_tile_offset) puts them on the CTAs with one tile fewer where it can, and a CTA's
+  // k = 0 tile comes last, so an edge tile is never the first one.
+  auto tile_ord = [&](int t) -> int64_t {
+    int64_t j = G.tile_off + blockIdx.x + (int64_t)(t + 1 < my_tiles ? t + 1 : 0) * gridDim.x;
+    return j >= G.ntiles ? j - G.ntiles : j;
+  };
+  auto P0_of = [&](int t) -> int64_t { return A.y_begin - G.shift + tile_ord(t) * TILE - (G.KT - 128); };
+  const int64_t P0_first = P0_of(0);
   auto staged = [&](int64_t P0) { return P0 >= 4 && P0 + 4 * (int64_t)G.nw4 + 4 <= A.n_in; };
   // one raw window: row s from dph[s] words earlier, so every source is 16-byte aligned
   auto issue_window = [&](int s, int64_t P0, int b) {
@@ -173,9 +206,12 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
   // quarter warp reads sit in different bank groups).  Lane v's 32 bytes of the
   // Toeplitz block of K step kc start at rev_j[32 kc + 127 - v].
   const int RL = G.KT + 144;
-  {
+  // (the converter warps go straight to the first tile's windows: they never read the taps)
+  const bool is_conv = warp >= CONV0 && warp < CONV0 + NCONV;
+  if (!is_conv) {
     const uint64_t gbias = bias_of(NG);
-    for (int i = tid; i < RL + NCOPY; i += NT) {
+    const int stid = warp < CONV0 ? tid : tid - 32 * NCONV;  // index among the NT - 32 NCONV staging threads
+    for (int i = stid; i < RL + NCOPY; i += NT - 32 * NCONV) {
       const int idx = G.KT - 1 - i;
       const int64_t gv = (idx >= 0 && idx < A.K) ? ld_bits(A.g, A.g_bits, idx) : 0;
       const uint64_t d = digits_of(gv, gbias);
@@ -187,10 +223,10 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
           if (i - k >= 0 && i - k < RL) rev[(j * NCOPY + k) * RL + (i - k)] = dj;
       }
     }
+    tc05::fence_before();
+    asm volatile("bar.sync 1, %0;" ::"n"(NT - 32 * NCONV) : "memory");
+    tc05::fence_after();
   }
-  tc05::fence_before();
-  __syncthreads();
-  tc05::fence_after();
   if (tmem_slot != 0 || (planes_s & 1023u)) __trap();
   constexpr uint32_t tbase = 0;
 
@@ -239,7 +275,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
       }
     };
     for (int t = 0; t < my_tiles; ++t) {
-      const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
+      const int64_t tile = tile_ord(t);
       const int64_t o0 = tile * TILE - G.shift + 128 * (EC * part) + v;
       uint32_t s0[EC], s1[EC], s2[EC];  // M_{P+1}; M_{P+2}, L_{P+2}
       {
@@ -290,12 +326,25 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
       int nbuf = 0;  // stream buffers filled so far
       for (int t = 0; t < my_tiles; ++t) {
         const int ts = t % NSLOT;
-        TM(0, mb_wait(full_b(ts), (uint32_t)((t / NSLOT) & 1)));
-        tc05::fence_after();
         if (elect_one()) {
           const uint32_t slot_s = planes_s + (uint32_t)(ts * SLOTB);
+#if !NENT_M4_WINBAR
+          for (int w = 0; w < M; ++w) TM(0, mb_wait(full_b(ts, w), (uint32_t)((t / NSLOT) & 1)));
+          tc05::fence_after();
+#endif
           for (int si = 0; si < nstr; ++si, ++nbuf) {
             const int i = (P + 1 + si) & 3, im1 = (i + M - 1) & 3;
+#if NENT_M4_WINBAR
+            // the byte planes of raw streams i and i-1 are in shared memory: the converters
+            // finish a tile's windows in the order 0, 1, 2, 3, so the later one is enough
+            TM(0, mb_wait(full_b(ts, i > im1 ? i : im1), (uint32_t)((t / NSLOT) & 1)));
+            tc05::fence_after();
+#endif
+            if (si == 0) {
+              if (t == 0) M4_STAMP(1);
+              if (t == 1) M4_STAMP(2);
+              if (t == my_tiles - 1) M4_STAMP(3);
+            }
             const int bsel = nbuf & 1;
             if (nbuf >= 2) {  // the stream that last used this buffer was drained
               TM(2, mb_wait(afree_b(bsel), (uint32_t)(((nbuf >> 1) - 1) & 1)));
@@ -396,86 +445,82 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
       }
     } else if (warp == LOAD_WARP) {
       // ---------------- loader ----------------
-      if (lane == 0) {
-        int64_t P0 = P0_first;
-        int issued = 0;
-        for (int t = 0; t < my_tiles; ++t, P0 += P0_step) {
-          if (!staged(P0)) continue;
+      // Every tile's four raw windows go through the staging ring.  A window inside the
+      // streams is ONE bulk copy issued by lane 0; a stream-edge window is copied by the whole
+      // warp with cp.async at phase 0 (conv_tc05.cuh: stage_edge_window), one window at a time,
+      // ahead of the converters and off their path.
+      int issued = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        const int64_t P0 = P0_of(t);
+        const bool whole = staged(P0);
 #pragma unroll
-          for (int s = 0; s < M; ++s) {
-            const int b = issued % NSTAGE;
-            if (!(pre_issue && issued < PRE)) {
-              if (issued >= NSTAGE) mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1));
-              issue_window(s, P0, b);
+        for (int s = 0; s < M; ++s) {
+          const int b = issued % NSTAGE;
+          if (!(pre_issue && issued < PRE)) {
+            if (issued >= NSTAGE) mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1));
+            if (whole) {
+              if (lane == 0) issue_window(s, P0, b);
+            } else {
+              tcc::stage_edge_window(stage_s + (uint32_t)b * SSTR, reinterpret_cast<const int32_t*>(A.b.p[s]), P0, A.n_in,
+                                     G.nw4, G.dph[s] == 0, lane);
+              asm volatile("cp.async.wait_all;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) mb_arrive(sfull_b(b));
             }
-            ++issued;
           }
+          ++issued;
         }
       }
     } else {
       // ---------------- converters ----------------
       const int cl = (warp - CONV0) * 32 + lane;  // converter lane 0 .. 63
-      int64_t P0 = P0_first;
       int consumed = 0;
-      for (int t = 0; t < my_tiles; ++t, P0 += P0_step) {
+      for (int t = 0; t < my_tiles; ++t) {
+        const int64_t P0 = P0_of(t);
         const int ts = t % NSLOT;
-        const bool fast = staged(P0);
+        const bool whole = staged(P0);
         if (t >= NSLOT) mb_wait_sleep(empty_b(ts), (uint32_t)(((t / NSLOT) - 1) & 1));
 #pragma unroll 1
         for (int s = 0; s < M; ++s) {
           const uint32_t plo = planes_s + (uint32_t)(ts * SLOTB + (2 * s) * PLANE);
-          if (fast) {
-            const int b = consumed % NSTAGE;
-            mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1));
-            const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
-            const int d = G.dph[s];
-            for (int q0 = cl; q0 < G.nw4; q0 += 4 * 32 * NCONV) {
-              int4 vv[4];
+          const int b = consumed % NSTAGE;
+          mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1));
+          const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
+          const int d = whole ? G.dph[s] : 0;  // (the loader stages a stream-edge window at phase 0)
+          for (int q0 = cl; q0 < G.nw4; q0 += 4 * 32 * NCONV) {
+            int4 vv[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int q = q0 + k * 32 * NCONV;
-                if (q < G.nw4) {
-                  if (d == 0) {
-                    vv[k] = lds128(sbuf + 16u * (uint32_t)q);
-                  } else {  // this row's window starts d words into the staged copy
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d + 4 * q;
-                    vv[k] = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
-                  }
-                }
-              }
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int q = q0 + k * 32 * NCONV;
-                if (q < G.nw4) {
-                  uint32_t lo, hi;
-                  split2(vv[k], lo, hi);
-                  const uint32_t off = tc05::sw128(4u * (uint32_t)q);
-                  sts32(plo + off, lo);
-                  sts32(plo + (uint32_t)PLANE + off, hi);
+            for (int k = 0; k < 4; ++k) {
+              const int q = q0 + k * 32 * NCONV;
+              if (q < G.nw4) {
+                if (d == 0) {
+                  vv[k] = lds128(sbuf + 16u * (uint32_t)q);
+                } else {  // this row's window starts d words into the staged copy
+                  const uint32_t* w = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d + 4 * q;
+                  vv[k] = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
                 }
               }
             }
-            __syncwarp();
-            if (lane == 0) mb_arrive(sfree_b(b));
-            ++consumed;
-          } else {
-            const int32_t* bp = reinterpret_cast<const int32_t*>(A.b.p[s]);
-            for (int q = cl; q < G.nw4; q += 32 * NCONV) {
-              const int64_t x0 = P0 + 4 * (int64_t)q;
-              int e[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) e[k] = (x0 + k >= 0 && x0 + k < A.n_in) ? __ldg(bp + x0 + k) : 0;
-              uint32_t lo, hi;
-              split2(make_int4(e[0], e[1], e[2], e[3]), lo, hi);
-              const uint32_t off = tc05::sw128(4u * (uint32_t)q);
-              sts32(plo + off, lo);
-              sts32(plo + (uint32_t)PLANE + off, hi);
+            for (int k = 0; k < 4; ++k) {
+              const int q = q0 + k * 32 * NCONV;
+              if (q < G.nw4) {
+                uint32_t lo, hi;
+                split2(vv[k], lo, hi);
+                const uint32_t off = tc05::sw128(4u * (uint32_t)q);
+                sts32(plo + off, lo);
+                sts32(plo + (uint32_t)PLANE + off, hi);
+              }
             }
           }
+          fence_async_smem();  // this thread's plane writes -> the MMA's async-proxy reads
+          __syncwarp();
+          if (lane == 0) {
+            mb_arrive(sfree_b(b));       // this warp's share of the staging buffer is read
+            mb_arrive(full_b(ts, s));    // ... and of the window's two planes written
+          }
+          ++consumed;
         }
-        fence_async_smem();  // this thread's plane writes -> the MMA's async-proxy reads
-        __syncwarp();
-        if (lane == 0) mb_arrive(full_b(ts));
       }
     }
   }
@@ -499,6 +544,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m4_kernel(const __grid_consta
   (void)tstart;
   tc05::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) M4_STAMP(4);
   if (warp == MMA_WARP) {
     tc05::fence_after();
     tc05::dealloc(tbase, 512);

@@ -47,6 +47,7 @@ int tc05_fused_m8(ConvArgs& A, int np, int ng, cudaStream_t s) {
                                  : (G.nsteps == 8 ? conv_tc05_m8_kernel<8> : conv_tc05_m8_kernel<12>);
   if (ensure_smem((const void*)kern, SMEM) != NENT_OK) return NENT_ERR_CUDA;
   const unsigned grid = (unsigned)(G.ntiles < sms ? G.ntiles : sms);
+  G.tile_off = edge_tile_offset(A.n_in, A.y_begin - G.shift - (G.KT - 128), 4 * (int64_t)G.nw4 + 4, TILE, G.ntiles, grid);
   kern<<<grid, NT, SMEM, s>>>(A, G);
   note_conv_kernel(6);
   return check_launch("tc05 fused m8");

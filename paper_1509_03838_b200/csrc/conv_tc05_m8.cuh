@@ -73,6 +73,7 @@ struct Geom {
   int KT, nsteps;
   int nw4;               // int4 words per raw window: (TILE + KT - 128) / 4
   int64_t ntiles;
+  int64_t tile_off;  // CTA b's tiles are (tile_off + b + k * grid) mod ntiles
   int shift;             // tiles start `shift` outputs early: row 0's windows are 16-byte aligned
   int dph[M];            // word phase of row s relative to row 0 (mod 4)
 };
@@ -119,8 +120,15 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m8_kernel(const __grid_consta
   if (tmem_slot != 0 || (planes_s & 1023u)) __trap();
   constexpr uint32_t tbase = 0;
   const int my_tiles = G.ntiles > blockIdx.x ? (int)((G.ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  const int64_t P0_first = A.y_begin - G.shift + (int64_t)blockIdx.x * TILE - (G.KT - 128);
-  const int64_t P0_step = (int64_t)gridDim.x * TILE;
+  // The CTA's tiles (tile_off + blockIdx.x + k * gridDim.x) mod ntiles are processed in the
+  // order k = 1, 2, ..., 0: the stream-edge tiles (staged by the loader warp with cp.async)
+  // sit on the CTAs with one tile fewer where they can (conv_common.cuh: edge_tile_offset)
+  // and are never a CTA's first tile.
+  auto tile_ord = [&](int t) -> int64_t {
+    int64_t j = G.tile_off + blockIdx.x + (int64_t)(t + 1 < my_tiles ? t + 1 : 0) * gridDim.x;
+    return j >= G.ntiles ? j - G.ntiles : j;
+  };
+  auto P0_of = [&](int t) -> int64_t { return A.y_begin - G.shift + tile_ord(t) * TILE - (G.KT - 128); };
   auto staged = [&](int64_t P0) { return P0 >= 4 && P0 + 4 * (int64_t)G.nw4 + 4 <= A.n_in; };
   {
     // the reversed taps (one signed digit), staged once in the (still free)
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m8_kernel(const __grid_consta
       for (int k = 0; k < EC; ++k) w[k] = a[k] + (b[k] << 8);
     };
     for (int t = 0; t < my_tiles; ++t) {
-      const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
+      const int64_t tile = tile_ord(t);
       const int64_t o0 = tile * TILE - G.shift + 128 * (EC * part) + v;
       uint32_t rot[M - 1][EC];  // rot[s] = delta_{(P+1+s) mod m}
 #pragma unroll
@@ -259,84 +267,80 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m8_kernel(const __grid_consta
       (void)spt;
     } else if (warp == LOAD_WARP) {
       // ---------------- loader ----------------
-      if (lane == 0) {
-        int64_t P0 = P0_first;
-        int issued = 0;
-        const uint32_t winb = 16u * (uint32_t)G.nw4;
-        for (int t = 0; t < my_tiles; ++t, P0 += P0_step) {
-          if (!staged(P0)) continue;
-          for (int s = 0; s < M; ++s) {
-            const int b = issued % NSTAGE;
-            if (issued >= NSTAGE) mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1));
-            const int d = G.dph[s];
-            const char* src = reinterpret_cast<const char*>(reinterpret_cast<const int32_t*>(A.b.p[s]) + P0 - d);
-            const uint32_t bytes = winb + (d ? 16u : 0u);
-            mb_expect_tx(sfull_b(b), bytes);
-            bulk_g2s(stage_s + (uint32_t)b * SSTR, src, bytes, sfull_b(b));
-            ++issued;
+      // Every tile's eight raw windows go through the staging ring: a window inside the
+      // streams is ONE bulk copy issued by lane 0, a stream-edge window is copied by the
+      // whole warp with cp.async at phase 0 (conv_tc05.cuh: stage_edge_window).
+      int issued = 0;
+      const uint32_t winb = 16u * (uint32_t)G.nw4;
+      for (int t = 0; t < my_tiles; ++t) {
+        const int64_t P0 = P0_of(t);
+        const bool whole = staged(P0);
+        for (int s = 0; s < M; ++s) {
+          const int b = issued % NSTAGE;
+          if (issued >= NSTAGE) mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1));
+          const int d = G.dph[s];
+          if (whole) {
+            if (lane == 0) {
+              const char* src = reinterpret_cast<const char*>(reinterpret_cast<const int32_t*>(A.b.p[s]) + P0 - d);
+              const uint32_t bytes = winb + (d ? 16u : 0u);
+              mb_expect_tx(sfull_b(b), bytes);
+              bulk_g2s(stage_s + (uint32_t)b * SSTR, src, bytes, sfull_b(b));
+            }
+          } else {
+            tcc::stage_edge_window(stage_s + (uint32_t)b * SSTR, reinterpret_cast<const int32_t*>(A.b.p[s]), P0, A.n_in,
+                                   G.nw4, d == 0, lane);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mb_arrive(sfull_b(b));
           }
+          ++issued;
         }
       }
     } else {
       // ---------------- converters ----------------
       const int cl = (warp - CONV0) * 32 + lane;  // converter lane 0 .. 191
-      int64_t P0 = P0_first;
       int consumed = 0;
-      for (int t = 0; t < my_tiles; ++t, P0 += P0_step) {
+      for (int t = 0; t < my_tiles; ++t) {
+        const int64_t P0 = P0_of(t);
         const int ts = t % NSLOT;
-        const bool fast = staged(P0);
+        const bool whole = staged(P0);
         if (t >= NSLOT) mb_wait_sleep(empty_b(ts), (uint32_t)(((t / NSLOT) - 1) & 1));
 #pragma unroll 1
         for (int s = 0; s < M; ++s) {
           const uint32_t plo = planes_s + (uint32_t)(ts * SLOTB + (2 * s) * PLANE);
-          if (fast) {
-            const int b = consumed % NSTAGE;
-            mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1));
-            const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
-            const int d = G.dph[s];
-            for (int q0 = cl; q0 < G.nw4; q0 += 3 * 32 * NCONV) {
-              int4 vv[3];
+          const int b = consumed % NSTAGE;
+          mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1));
+          const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
+          const int d = whole ? G.dph[s] : 0;  // (the loader stages a stream-edge window at phase 0)
+          for (int q0 = cl; q0 < G.nw4; q0 += 3 * 32 * NCONV) {
+            int4 vv[3];
 #pragma unroll
-              for (int k = 0; k < 3; ++k) {
-                const int q = q0 + k * 32 * NCONV;
-                if (q < G.nw4) {
-                  if (d == 0) {
-                    vv[k] = lds128(sbuf + 16u * (uint32_t)q);
-                  } else {  // this row's window starts d words into the staged copy
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d + 4 * q;
-                    vv[k] = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
-                  }
-                }
-              }
-#pragma unroll
-              for (int k = 0; k < 3; ++k) {
-                const int q = q0 + k * 32 * NCONV;
-                if (q < G.nw4) {
-                  uint32_t lo, hi;
-                  split2(vv[k], lo, hi);
-                  const uint32_t off = tc05::sw128(4u * (uint32_t)q);
-                  sts32(plo + off, lo);
-                  sts32(plo + (uint32_t)PLANE + off, hi);
+            for (int k = 0; k < 3; ++k) {
+              const int q = q0 + k * 32 * NCONV;
+              if (q < G.nw4) {
+                if (d == 0) {
+                  vv[k] = lds128(sbuf + 16u * (uint32_t)q);
+                } else {  // this row's window starts d words into the staged copy
+                  const uint32_t* w = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d + 4 * q;
+                  vv[k] = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
                 }
               }
             }
-            __syncwarp();
-            if (lane == 0) mb_arrive(sfree_b(b));
-            ++consumed;
-          } else {
-            const int32_t* bp = reinterpret_cast<const int32_t*>(A.b.p[s]);
-            for (int q = cl; q < G.nw4; q += 32 * NCONV) {
-              const int64_t x0 = P0 + 4 * (int64_t)q;
-              int e[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) e[k] = (x0 + k >= 0 && x0 + k < A.n_in) ? __ldg(bp + x0 + k) : 0;
-              uint32_t lo, hi;
-              split2(make_int4(e[0], e[1], e[2], e[3]), lo, hi);
-              const uint32_t off = tc05::sw128(4u * (uint32_t)q);
-              sts32(plo + off, lo);
-              sts32(plo + (uint32_t)PLANE + off, hi);
+            for (int k = 0; k < 3; ++k) {
+              const int q = q0 + k * 32 * NCONV;
+              if (q < G.nw4) {
+                uint32_t lo, hi;
+                split2(vv[k], lo, hi);
+                const uint32_t off = tc05::sw128(4u * (uint32_t)q);
+                sts32(plo + off, lo);
+                sts32(plo + (uint32_t)PLANE + off, hi);
+              }
             }
           }
+          __syncwarp();
+          if (lane == 0) mb_arrive(sfree_b(b));
+          ++consumed;
         }
         fence_async_smem();  // this thread's plane writes -> the MMA's async-proxy reads
         __syncwarp();

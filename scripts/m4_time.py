@@ -9,7 +9,10 @@ from paper_1509_03838_b200 import _device as D  # noqa: E402
 from paper_1509_03838_b200 import workloads  # noqa: E402
 from paper_1509_03838_b200._lib import imma_flavor  # noqa: E402
 
+import os  # noqa: E402
+
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+dump = "--dump" in sys.argv  # stamps builds (-DNENT_M4_STAMPS): the timeline of one more back-to-back launch
 wl = workloads.make(3)
 n, K, p = wl.n, wl.K, wl.params
 L = n + K - 1
@@ -27,6 +30,10 @@ for r in (None, 1):
     for _ in range(reps):
         f()
     e1.record()
+    if dump:
+        os.environ["NENT_M4_DUMP"] = "1"
+        f()
+        del os.environ["NENT_M4_DUMP"]
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     macs = 4 * n * K * 8 * (1 if r is None else 0.75)

@@ -356,10 +356,16 @@ def run_ours(args):
         "entangled_cuda_core": lambda: fused_step(core_flavor),
         "plain_cuda_core_same_width": lambda: plain(core_flavor),
     }
+    # every launch timed on its own, the candidates' order rotated from round to round: what a
+    # launch costs depends on its predecessor (behind the 1 ms F64 kernels, whose int64 output
+    # is still being written back from L2, the m = 3 kernel's first tiles take 5 us longer), so
+    # each candidate gets each position equally often
     evs = {k: [] for k in cands}
-    for _ in range(max(5, min(args.steps, 11))):
-        for k, fn in cands.items():
-            evs[k].append(event_time(fn, stream))
+    names = list(cands)
+    for rnd in range(len(names) * (2 if args.steps >= 12 else 1)):
+        for j in range(len(names)):
+            k = names[(j + rnd) % len(names)]
+            evs[k].append(event_time(cands[k], stream))
     torch.cuda.synchronize(dev)
     t = {k: [a.elapsed_time(b) for a, b in v] for k, v in evs.items()}
     med = {k: statistics.median(v) for k, v in t.items()}

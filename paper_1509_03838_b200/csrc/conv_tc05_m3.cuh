@@ -106,7 +106,6 @@ constexpr int EPI_REGS = NENT_M3_EPI_REGS, PROD_REGS = 256 - EPI_REGS;
 static_assert(EPI_REGS % 8 == 0 && PROD_REGS >= 40, "setmaxnreg granularity");
 static_assert(NEPI * 32 * EPI_REGS + (NT / 32 - NEPI) * 32 * PROD_REGS <= NT * LAUNCH_REGS, "launch register pool");
 static_assert(NEPI % 4 == 0 && (NT / 32 - NEPI) % 4 == 0, "setmaxnreg acts on whole warpgroups");
-static_assert(NSTAGE >= 3, "a stream-edge tile's three windows are staged together");
 static_assert(NSLOT >= 2, "the taps' digits are staged in the last plane slot while the first tile is split into slot 0");
 static_assert(4 * NWP >= TILE + 256, "a staged window covers the tile plus the K <= 257 halo");
 static_assert(4 * NWP <= PLANE, "a staged window fits its plane");
@@ -527,7 +526,11 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PROD_REGS));
     // per-stream operands by select (a runtime-indexed array would live in local memory)
     const int dph0 = G.dph[0], dph1 = G.dph[1], dph2 = G.dph[2];
+    const int32_t* row0 = reinterpret_cast<const int32_t*>(A.b.p[0]);
+    const int32_t* row1 = reinterpret_cast<const int32_t*>(A.b.p[1]);
+    const int32_t* row2 = reinterpret_cast<const int32_t*>(A.b.p[2]);
     auto dph_of = [&](int k) { return k == 0 ? dph0 : (k == 1 ? dph1 : dph2); };
+    auto row_of = [&](int k) { return k == 0 ? row0 : (k == 1 ? row1 : row2); };
     if (warp == MMA_WARP) {
       // ---------------- MMA issuer ----------------
       // B operand signedness per data digit: low bytes unsigned, high bytes signed
@@ -631,36 +634,21 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       if (lane == 0) STAMP(7);
     } else if (warp == LOAD_WARP) {
       // ---------------- loader ----------------
-      // Every tile's three raw windows go through the staging ring as soon as a buffer is
-      // free (the first PRE went out above).  A window inside the streams is ONE bulk copy
-      // issued by lane 0; a stream-edge window is copied by the whole warp with cp.async
-      // (16 bytes where the int4 is aligned and inside the stream or wholly outside it,
-      // else sample by sample with zero fill), at phase 0 -- one tile ahead of the converters, off their path.
-      int issued = 0;
-      for (int t = 0; t < my_tiles; ++t) {
-        const int64_t P0 = P0_of(t);
-        const bool whole = staged(P0);
+      // One thread: every staged tile's three raw windows, one bulk copy each,
+      // as soon as a staging buffer is free (the first PRE went out above).
+      if (lane == 0) {
+        int issued = 0;
+        for (int t = 0; t < my_tiles; ++t) {
+          const int64_t P0 = P0_of(t);
+          if (!staged(P0)) continue;
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          const int b = issued % NSTAGE;
-          if (!(pre_issue && issued < PRE)) {
-            if (issued >= NSTAGE) TM(0, mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1)));
-            if (whole) {
-              if (lane == 0) issue_window(s, P0, b);
-            } else {
-              tcc::stage_edge_window(stage_s + (uint32_t)b * SSTR, reinterpret_cast<const int32_t*>(A.b.p[s]), P0, A.n_in,
-                                     NWP, G.dph[s] == 0, lane);
+          for (int s = 0; s < 3; ++s) {
+            const int b = issued % NSTAGE;
+            if (!(pre_issue && issued < PRE)) {
+              if (issued >= NSTAGE) TM(0, mb_wait_sleep(sfree_b(b), (uint32_t)(((issued / NSTAGE) - 1) & 1)));
+              issue_window(s, P0, b);
             }
-          }
-          ++issued;
-        }
-        if (!whole) {
-          // one wait for the tile's three windows, then their three arrivals
-          asm volatile("cp.async.wait_all;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-#pragma unroll
-            for (int s = 0; s < 3; ++s) mb_arrive(sfull_b((issued - 3 + s) % NSTAGE));
+            ++issued;
           }
         }
       }
@@ -674,7 +662,7 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
       for (int t = 0; t < my_tiles; ++t) {
         const int64_t P0 = P0_of(t);
         const int ts = t % NSLOT;
-        const bool whole = staged(P0);
+        const bool fast = staged(P0);
         // the tap builders are done with the digits staged in the last plane slot
         if (t == NSLOT - 1) asm volatile("bar.sync 2, %0;" ::"n"(TAPBAR) : "memory");
         // the MMAs that read this plane slot NSLOT tiles ago are done
@@ -682,52 +670,78 @@ __global__ void __launch_bounds__(NT, 1) conv_tc05_m3_kernel(const __grid_consta
 #pragma unroll 1
         for (int s = 0; s < 3; ++s) {
           const uint32_t plo = planes_s + (uint32_t)(ts * SLOTB + (2 * s) * PLANE);
-          const int b = consumed % NSTAGE;
-          TM(1, mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1)));
-          if (t == 0 && cw == 0 && lane == 0) STAMP(10 + s);
-          const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
-          const int d = whole ? dph_of(s) : 0;  // (the loader stages a stream-edge window at phase 0)
-          {
-            TM_BEGIN();
-            if (d == 0) {
-              const uint32_t la = sbuf + 16u * (uint32_t)(wbase + lane);
-              // two batches of loads (6 + 5 words): 24 registers in flight
-              constexpr int BW = (WW + 1) / 2;
+          if (fast) {
+            const int b = consumed % NSTAGE;
+            TM(1, mb_wait_sleep(sfull_b(b), (uint32_t)((consumed / NSTAGE) & 1)));
+            if (t == 0 && cw == 0 && lane == 0) STAMP(10 + s);
+            const uint32_t sbuf = stage_s + (uint32_t)b * SSTR;
+            const int d = dph_of(s);
+            {
+              TM_BEGIN();
+              if (d == 0) {
+                const uint32_t la = sbuf + 16u * (uint32_t)(wbase + lane);
+                // two batches of loads (6 + 5 words): 24 registers in flight
+                constexpr int BW = (WW + 1) / 2;
 #pragma unroll
-              for (int i0 = 0; i0 < WW; i0 += BW) {
-                int4 v[BW];
+                for (int i0 = 0; i0 < WW; i0 += BW) {
+                  int4 v[BW];
 #pragma unroll
-                for (int i = 0; i < BW; ++i)
-                  if (i0 + i < WW) v[i] = lds128(la + 512u * (uint32_t)(i0 + i));
+                  for (int i = 0; i < BW; ++i)
+                    if (i0 + i < WW) v[i] = lds128(la + 512u * (uint32_t)(i0 + i));
 #pragma unroll
-                for (int i = 0; i < BW; ++i)
-                  if (i0 + i < WW) {
-                    uint32_t lo, hi;
-                    split2(v[i], lo, hi);
-                    const uint32_t off = soff(i0 + i);
-                    sts32(plo + off, lo);
-                    sts32(plo + (uint32_t)PLANE + off, hi);
-                  }
+                  for (int i = 0; i < BW; ++i)
+                    if (i0 + i < WW) {
+                      uint32_t lo, hi;
+                      split2(v[i], lo, hi);
+                      const uint32_t off = soff(i0 + i);
+                      sts32(plo + off, lo);
+                      sts32(plo + (uint32_t)PLANE + off, hi);
+                    }
+                }
+              } else {  // this row's window starts d words into the staged copy
+                const uint32_t* sw = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d;
+#pragma unroll
+                for (int i = 0; i < WW; ++i) {
+                  const uint32_t* q = sw + 4 * (wbase + 32 * i + lane);
+                  uint32_t lo, hi;
+                  split2(make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]), lo, hi);
+                  const uint32_t off = soff(i);
+                  sts32(plo + off, lo);
+                  sts32(plo + (uint32_t)PLANE + off, hi);
+                }
               }
-            } else {  // this row's window starts d words into the staged copy
-              const uint32_t* sw = reinterpret_cast<const uint32_t*>(__cvta_shared_to_generic(sbuf)) + d;
-#pragma unroll
-              for (int i = 0; i < WW; ++i) {
-                const uint32_t* q = sw + 4 * (wbase + 32 * i + lane);
-                uint32_t lo, hi;
-                split2(make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]), lo, hi);
-                const uint32_t off = soff(i);
-                sts32(plo + off, lo);
-                sts32(plo + (uint32_t)PLANE + off, hi);
-              }
+              TM_END(4);
             }
-            TM_END(4);
+            // this warp's reads of the staging buffer are complete (their
+            // values were stored): hand its share back to the loader
+            __syncwarp();
+            if (lane == 0) mb_arrive(sfree_b(b));
+            ++consumed;
+          } else {
+            // a stream-edge tile: element loads with zero extension, in the same two batches
+            const int32_t* bp = row_of(s);
+            constexpr int BW = (WW + 1) / 2;
+#pragma unroll
+            for (int i0 = 0; i0 < WW; i0 += BW) {
+              int e[BW][4];
+#pragma unroll
+              for (int i = 0; i < BW; ++i)
+                if (i0 + i < WW) {
+                  const int64_t q0 = P0 + 4 * (int64_t)(wbase + 32 * (i0 + i) + lane);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) e[i][k] = (q0 + k >= 0 && q0 + k < A.n_in) ? __ldg(bp + q0 + k) : 0;
+                }
+#pragma unroll
+              for (int i = 0; i < BW; ++i)
+                if (i0 + i < WW) {
+                  uint32_t lo, hi;
+                  split2(make_int4(e[i][0], e[i][1], e[i][2], e[i][3]), lo, hi);
+                  const uint32_t off = soff(i0 + i);
+                  sts32(plo + off, lo);
+                  sts32(plo + (uint32_t)PLANE + off, hi);
+                }
+            }
           }
-          // this warp's reads of the staging buffer are complete (their
-          // values were stored): hand its share back to the loader
-          __syncwarp();
-          if (lane == 0) mb_arrive(sfree_b(b));
-          ++consumed;
         }
         // the tile's planes are complete (this warp's share)
         fence_async_smem();  // this thread's plane writes -> the MMA's async-proxy reads

@@ -26,3 +26,20 @@ $CMD3 > gpurun_out/${TAG}_plain3.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:conv_tc05_m4 -s 2 -c 1 \
     -o gpurun_out/${TAG}_prof_m4 $CMD3 > gpurun_out/${TAG}_ncu_full_m4.log 2>&1
 echo "full m4 rc=$?" >> gpurun_out/${TAG}_plain3.log
+# per-CTA timelines (stamps builds, scripts/build_variant.py), the old-vs-new A/B when the
+# previous build's library is there, and the NVML power / clock probe
+if [ -f scripts/_bin/libnent_b200_stamps.so ]; then
+  timeout 120 python scripts/with_variant.py libnent_b200_stamps.so scripts/m3_time.py 50 --dump > gpurun_out/${TAG}_timeline_m3.log 2>&1
+fi
+if [ -f scripts/_bin/libnent_b200_stamps4.so ]; then
+  timeout 120 python scripts/with_variant.py libnent_b200_stamps4.so scripts/m4_time.py 50 --dump > gpurun_out/${TAG}_timeline_m4.log 2>&1
+fi
+if [ -f scripts/_bin/libnent_b200_old.so ]; then
+  for i in 1 2; do
+    echo "previous build (r02e)"; timeout 120 python scripts/with_variant.py libnent_b200_old.so scripts/m3_time.py 200
+    echo "this build"; timeout 120 python scripts/m3_time.py 200
+  done > gpurun_out/${TAG}_ab_m3.log 2>&1
+fi
+timeout 120 python scripts/m4_time.py 200 > gpurun_out/${TAG}_time_m4_m8.log 2>&1
+timeout 120 python scripts/m8_time.py 100 >> gpurun_out/${TAG}_time_m4_m8.log 2>&1
+timeout 120 python scripts/power_probe.py 4 > gpurun_out/${TAG}_power.log 2>&1

@@ -88,7 +88,7 @@ def device_to_host(t: torch.Tensor) -> np.ndarray:
     """Device tensor -> a fresh numpy array (what ``t.cpu().numpy()`` returns)."""
     nbytes = t.numel() * t.element_size()
     if not t.is_cuda or not STAGE_MIN <= nbytes <= STAGE_MAX:
-        return t.cpu().numpy()
+        return t.contiguous().cpu().numpy()  # (row-padded results are compacted first)
     with _stage_lock["out"]:
         stage = _staging("out", nbytes).view(t.dtype).reshape(t.shape)  # pinned
         stage.copy_(t, non_blocking=True)
@@ -110,6 +110,14 @@ def as_device(data, dtype=torch.int64) -> torch.Tensor:
     arr = np.ascontiguousarray(data, dtype=np.int64)
     t = host_to_device(arr, dev)
     return t if dtype in (None, torch.int64) else t.to(dtype)
+
+
+def alloc_rows(m: int, n: int, dtype, dev) -> torch.Tensor:
+    """(m, n) device tensor whose rows start 128-byte aligned (a padded row pitch): the
+    convolution kernels' warps then store whole 128-byte lines on every row.  The C ABI takes
+    one pointer per row, so a row pitch is free."""
+    q = 128 // torch.empty((), dtype=dtype).element_size()
+    return torch.empty((m, -(-n // q) * q), dtype=dtype, device=dev)[:, :n]
 
 
 def _status() -> torch.Tensor:
@@ -291,7 +299,7 @@ def conv(x: torch.Tensor, g_dev: torch.Tensor, K: int, flavor: int, period: int 
     period = n_in if period is None else period
     n_out = period if n_out is None else n_out
     if out is None:
-        out = torch.empty((rows, n_out), dtype=out_dtype, device=x.device)
+        out = alloc_rows(rows, n_out, out_dtype, x.device)
     ovf = _status() if flavor == MAC_X128 else None
     if x.dtype == torch.int32 and flavor in (MAC_G64, MAC_X128):
         x = x.to(torch.int64)
@@ -316,7 +324,7 @@ def fused_conv(c, g_dev: torch.Tensor, K: int, l: int, flavor: int, r: int | Non
     n_in = rows[0].shape[-1] if n_in is None else n_in
     n_out = period if n_out is None else n_out
     if out is None:
-        out = torch.empty((m, n_out), dtype=out_dtype, device=rows[0].device)
+        out = alloc_rows(m, n_out, out_dtype, rows[0].device)
     call("nent_fused_conv", row_ptrs(rows), bits(rows[0]), m, n_in, period, l, int(scale),
          ptr(add), bits(add) if add is not None else 64, ptr(perm), ptr(g_dev), bits(g_dev), K,
          -1 if r is None else int(r), int(bool(pre_entangled)), row_ptrs(out), bits(out), y_begin,

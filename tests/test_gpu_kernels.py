@@ -694,3 +694,42 @@ def test_k1_k3_vectorised_and_scalar_paths(oracle, m, w, n, off):
     for (i, j) in ((m - 1, n - 1), (1, n // 2), (1, n // 2 + 1)):
         x[i, j] = lim + 1
     assert D.entangle(x, p.l, check_hi=lim)[1] == 1 * n + n // 2
+
+
+@pytest.mark.parametrize("kern", ["m3", "m4", "m8"])
+def test_tcgen05_edge_tiles_on_multi_tile_ctas(oracle, kern):
+    """More tiles than SMs, a tile count that is not a multiple of the grid, rows at
+    different 16-byte phases and output windows: the persistent kernels' tile order
+    (conv_common.cuh: edge_tile_offset -- the stream-edge tiles last in a CTA's order and on
+    the CTAs with one tile fewer) and the edge windows' staging paths (the loader warp's
+    cp.async copies with zero fill in the m = 4 / m = 8 kernels, the converters' element
+    loads in the m = 3 kernel), every failure case, against the oracle."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    if kern == "m3":
+        m, w, tile, K, lim, pre = 3, 48, 8192, 200, 2047, False
+    elif kern == "m4":
+        m, w, tile, K, lim, pre = 4, 64, 4096, 300, 511, False
+    else:
+        m, w, tile, K, lim, pre = 8, 32, 4096, 100, 7, True
+    n = (sms + 5) * tile + 1237  # sms + 6 or sms + 7 tiles
+    p = nent.derive_params(m, w)
+    glim = 3 if pre else lim
+    c = rand(n % 1000 + m, (m, n), -lim - 1, lim)
+    g = rand(n % 1000 + m + 1, (K,), -glim, glim)
+    ref = oracle.full_conv(c, g)
+    src = oracle.entangle(c, p.l) if pre else c
+    big = torch.zeros((m, n + 9), dtype=torch.int32, device="cuda")  # odd pitch: every row another phase
+    big[:, 1:1 + n] = torch.from_numpy(src).to(torch.int32)
+    x = big[:, 1:1 + n]
+    L = n + K - 1
+    fl = imma_flavor(2, 1) if pre else imma_flavor(4, 2)
+    gd = D.taps_tensor(g, fl)
+    for y0, cnt in [(0, L), (3, L - 3), (tile + 5, L - 2 * tile)]:
+        for r in [None] + list(range(m)):
+            mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+            out = torch.full((m, cnt), -7, dtype=torch.int32, device="cuda")
+            D.fused_conv(x, gd, K, p.l, fl, r, w > 32, L, n_in=n, y_begin=y0, n_out=cnt, out=out,
+                         mismatch=mm if r is None else None, pre_entangled=pre)
+            assert D.last_conv_kernel() == "tcgen05_" + kern
+            assert np.array_equal(out.to(torch.int64).cpu().numpy(), ref[:, y0:y0 + cnt]), (kern, y0, cnt, r)
+            assert int(mm.item()) == 0

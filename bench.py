@@ -126,6 +126,7 @@ class ClockSampler:
     def __init__(self, index: int, period_s: float = 0.002):
         self.index, self.period = index, period_s
         self.samples: list[int] = []
+        self.power_w: list[float] = []
         self.reasons: set[str] = set()
         self.max_mhz = None
         self.source = "nvml"
@@ -144,6 +145,10 @@ class ClockSampler:
                 while not self._stop.is_set():
                     self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
                     bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    try:
+                        self.power_w.append(N.nvmlDeviceGetPowerUsage(h) / 1e3)
+                    except Exception:
+                        pass
                     for nm, mask in masks:
                         if bits & mask:
                             self.reasons.add(nm)
@@ -173,7 +178,11 @@ class ClockSampler:
         sm = self.samples
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(sm), "source": self.source,
-                "sm_mhz_min": min(sm) if sm else None}
+                "sm_mhz_min": min(sm) if sm else None,
+                # NVML's board power over the same samples (its averaging window is longer than
+                # the timed region: run for seconds the headline kernel sits at the 1,000 W limit
+                # with sw_power_cap set)
+                "power_w_max": max(self.power_w) if self.power_w else None}
 
 
 # -------------------------------------------------------------- workload --

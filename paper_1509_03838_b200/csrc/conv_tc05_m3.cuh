@@ -30,9 +30,11 @@
 // CTA: 16 warps = 4 warpgroups, one persistent CTA per SM; a tile is 64
 // blocks of 128 outputs (MMA N = 64) of each stream.
 //   warps 0-7   epilogue (2 per TMEM lane quadrant, 32 accumulator columns
-//               each; more registers after setmaxnreg)
+//               each; more registers after setmaxnreg); they first build the
+//               tap table in TMEM, beside the first tile's conversion
 //   warps 8-13  converters: each splits its 1/6 of every staged raw window
-//               into the two byte planes (2 tile slots)
+//               into the two byte planes (2 tile slots); a stream-edge tile's
+//               windows are loaded element by element with zero extension
 //   warp 14     loader: one thread TMA-copies every raw int32 window (33 KB)
 //               into a ring of staging buffers
 //   warp 15     TMEM allocation; one elected lane issues every tcgen05.mma

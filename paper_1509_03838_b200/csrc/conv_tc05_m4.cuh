@@ -36,7 +36,8 @@
 //   warps 0-7   epilogue (2 per TMEM lane quadrant, 16 accumulator columns each)
 //   warps 8-11  tap writers
 //   warps 12-13 converters (raw int32 window -> two byte planes per stream)
-//   warp 14     loader: one thread, one bulk copy per raw window
+//   warp 14     loader: lane 0 issues one bulk copy per raw window; a stream-edge window (not
+//               wholly inside the stream) is staged by the whole warp with cp.async + zero fill
 //   warp 15     TMEM allocation; one elected lane issues every tcgen05.mma
 // Extraction: the streams are convolved in the order P+1, P+2, P+3 (and P last
 // when all four are present and the redundant one is checked), P the failed

@@ -23,7 +23,8 @@
 // tile is 32 blocks of 128 outputs (MMA 128 x 32 x 32) of each row:
 //   warps 0-7   epilogue (2 per TMEM lane quadrant, 16 accumulator columns each)
 //   warps 8-13  converters (raw int32 window -> two byte planes per row)
-//   warp 14     loader: one thread, one bulk copy per raw window
+//   warp 14     loader: lane 0 issues one bulk copy per raw window; a stream-edge window (not
+//               wholly inside the stream) is staged by the whole warp with cp.async + zero fill
 //   warp 15     TMEM allocation; one elected lane issues every tcgen05.mma
 // TMEM: tap digits in columns [0, 96), a ring of 13 accumulator slots of 32.
 #pragma once
